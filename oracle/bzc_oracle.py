@@ -437,7 +437,7 @@ def gradient_array(shape) -> np.ndarray:
 # ---------------------------------------------------------- tie handling ----
 
 def tie_mask(coeffs: np.ndarray, maxima: np.ndarray, d: int, index_kind: str,
-             window: float = 2.0 ** -30) -> np.ndarray:
+             window: float = 2.0 ** -36) -> np.ndarray:
     """Coefficients whose pre-rounding bin value sits near a half-integer.
 
     v = (C / N) * r is the value the reference rounds (codec.py:272-277).

@@ -1,0 +1,247 @@
+// bz_api.cu -- extern "C" entry points (include/bzc_b200.h).
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "bz_common.cuh"
+#include "bz_kernels.cuh"
+
+namespace bz {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return BZ_E_CUDA;
+  }
+  return BZ_OK;
+}
+
+static int validate(const bz_layout* L) {
+  if (!L || L->ndim < 1 || L->ndim > BZ_MAX_DIMS) { set_error("layout: ndim out of range"); return BZ_E_INVALID; }
+  if (L->float_kind < 0 || L->float_kind > 3 || L->index_kind < 0 || L->index_kind > 3) { set_error("layout: bad kind"); return BZ_E_INVALID; }
+  int bs = 1;
+  for (int a = 0; a < L->ndim; ++a) {
+    if (L->block[a] < 1 || (L->block[a] & (L->block[a] - 1))) { set_error("layout: block extents must be powers of two"); return BZ_E_INVALID; }
+    if (L->shape[a] < 1) { set_error("layout: zero extent"); return BZ_E_INVALID; }
+    if (L->grid[a] != (L->shape[a] + L->block[a] - 1) / L->block[a]) { set_error("layout: grid != ceil(shape/block)"); return BZ_E_INVALID; }
+    bs *= L->block[a];
+  }
+  if (L->kept < 0 || L->kept > bs) { set_error("layout: kept out of range"); return BZ_E_INVALID; }
+  if (L->kept > 0 && (!L->kept_pos || !L->rank)) { set_error("layout: mask tables missing"); return BZ_E_INVALID; }
+  return BZ_OK;
+}
+
+// BZC_B200_FORCE_GENERIC=1 routes compress/decompress through the exact
+// generic kernels (testing: fast vs generic agreement)
+static bool force_generic() {
+  const char* v = getenv("BZC_B200_FORCE_GENERIC");
+  return v && v[0] == '1';
+}
+
+static int need_matrices(const bz_layout* L) {
+  if (!L->matrices) { set_error("layout: transform matrices missing"); return BZ_E_INVALID; }
+  return BZ_OK;
+}
+
+}  // namespace bz
+
+using namespace bz;
+
+#define S(stream) reinterpret_cast<cudaStream_t>(stream)
+
+extern "C" {
+
+int bz_version(void) { return 10000; }
+const char* bz_last_error(void) { return g_err; }
+
+int bz_fast_path(const bz_layout* L) {
+  if (validate(L)) return 0;
+  Geo g = make_geo(L);
+  return fast_supported(g, L->float_kind) ? 1 : 0;
+}
+
+// workspace for compress: special-block counter + list (fast path), or the
+// generic kernel's global scratch, or a pre-rounded copy of the input when its
+// kind differs from the float kind.
+size_t bz_compress_workspace(const bz_layout* L) {
+  if (validate(L)) return 0;
+  Geo g = make_geo(L);
+  size_t list = 16 + (size_t)g.nblocks * sizeof(int32_t);
+  size_t generic = exact_compress_workspace(g, g.nblocks);
+  size_t convert = (size_t)dense_count(L) * float_kind_bytes(L->float_kind) + 256;
+  return list + std::max(generic, convert) + 256;
+}
+
+int bz_compress(const bz_layout* L, const void* x, int x_kind, void* maxima, void* indices,
+                void* ws, size_t ws_bytes, void* stream) {
+  if (int rc = validate(L)) return rc;
+  if (int rc = need_matrices(L)) return rc;
+  Geo g = make_geo(L);
+  if (g.nblocks == 0) return BZ_OK;
+  cudaStream_t s = S(stream);
+  size_t list_bytes = 16 + (size_t)g.nblocks * sizeof(int32_t);
+  if (!ws || ws_bytes < list_bytes) { set_error("compress: workspace too small"); return BZ_E_WORKSPACE; }
+  int32_t* cnt = reinterpret_cast<int32_t*>(ws);
+  int32_t* list = cnt + 4;
+  unsigned char* rest = reinterpret_cast<unsigned char*>(ws) + ((list_bytes + 255) / 256) * 256;
+  size_t rest_bytes = ws_bytes - (rest - reinterpret_cast<unsigned char*>(ws));
+  const void* src = x;
+  int src_kind = x_kind;
+  // input of another kind: convert_precision first (arrays.py:147-153)
+  if (x_kind != L->float_kind && !force_generic() &&
+      fast_supported(g, L->float_kind) && (L->float_kind == BZ_F32 || L->float_kind == BZ_F64)) {
+    size_t need = (size_t)dense_count(L) * float_kind_bytes(L->float_kind);
+    if (rest_bytes < need) { set_error("compress: workspace too small for conversion"); return BZ_E_WORKSPACE; }
+    if (int rc = launch_round_to_kind(x, x_kind, rest, L->float_kind, dense_count(L), nullptr, s)) return rc;
+    src = rest;
+    src_kind = L->float_kind;
+    rest += ((need + 255) / 256) * 256;
+    rest_bytes = ws_bytes - (rest - reinterpret_cast<unsigned char*>(ws));
+  }
+  if (!force_generic() && fast_supported(g, src_kind)) {
+    if (cudaMemsetAsync(cnt, 0, sizeof(int32_t), s) != cudaSuccess) return check_launch("memset");
+    if (int rc = launch_fast_compress(g, src, maxima, indices, cnt, list, s)) return rc;
+    // exact recomputation of flagged blocks (usually none)
+    return launch_exact_compress(g, src, src_kind, maxima, indices, list, cnt, g.nblocks / 64 + 1,
+                                 rest, rest_bytes, s);
+  }
+  return launch_exact_compress(g, x, x_kind, maxima, indices, nullptr, nullptr, g.nblocks, rest,
+                               rest_bytes, s);
+}
+
+size_t bz_decompress_workspace(const bz_layout* L) {
+  if (validate(L)) return 0;
+  Geo g = make_geo(L);
+  return exact_compress_workspace(g, g.nblocks) + 256;
+}
+
+int bz_decompress(const bz_layout* L, const void* maxima, const void* indices, void* out,
+                  int out_kind, void* ws, size_t ws_bytes, void* stream) {
+  if (int rc = validate(L)) return rc;
+  if (int rc = need_matrices(L)) return rc;
+  Geo g = make_geo(L);
+  if (g.nblocks == 0) return BZ_OK;
+  if (!force_generic() && fast_decompress_supported(g, out_kind))
+    return launch_fast_decompress(g, maxima, indices, out, out_kind, S(stream));
+  return launch_exact_decompress(g, maxima, indices, out, out_kind, ws, ws_bytes, S(stream));
+}
+
+int bz_negate(int index_kind, const void* in, void* out, int64_t count, void* stream) {
+  if (index_kind < 0 || index_kind > 3) { set_error("negate: bad index kind"); return BZ_E_INVALID; }
+  return launch_negate(index_kind, in, out, count, S(stream));
+}
+
+int bz_mul_scalar(const bz_layout* L, const void* maxima, const void* indices, double x,
+                  void* maxima_out, void* indices_out, void* stream) {
+  if (int rc = validate(L)) return rc;
+  return launch_mul_scalar(make_geo(L), maxima, indices, x, maxima_out, indices_out, S(stream));
+}
+
+int bz_add(const bz_layout* La, const bz_layout* Lb, const void* a_max, const void* a_idx,
+           const void* b_max, const void* b_idx, int subtract, void* out_max, void* out_idx,
+           void* stream) {
+  if (int rc = validate(La)) return rc;
+  if (int rc = validate(Lb)) return rc;
+  if (La->index_kind != Lb->index_kind || La->kept != Lb->kept) { set_error("add: incompatible operands"); return BZ_E_INVALID; }
+  return launch_add(make_geo(La), make_geo(Lb), a_max, a_idx, b_max, b_idx, subtract, 0.0, 0,
+                    out_max, out_idx, S(stream));
+}
+
+int bz_add_scalar(const bz_layout* L, const void* maxima, const void* indices, double shift,
+                  void* out_max, void* out_idx, void* stream) {
+  if (int rc = validate(L)) return rc;
+  if (!L->keeps_first) { set_error("add_scalar: mask drops the first coefficient"); return BZ_E_INVALID; }
+  Geo g = make_geo(L);
+  return launch_add(g, g, maxima, indices, nullptr, nullptr, 0, shift, 1, out_max, out_idx,
+                    S(stream));
+}
+
+size_t bz_moments_workspace(const bz_layout* L) {
+  if (validate(L)) return 0;
+  return moments_workspace(make_geo(L));
+}
+
+int bz_moments(const bz_layout* La, const bz_layout* Lb, const void* a_max, const void* a_idx,
+               const void* b_max, const void* b_idx, int pair, int dc_only, double* record,
+               void* ws, size_t ws_bytes, void* stream) {
+  if (int rc = validate(La)) return rc;
+  const bz_layout* lb = pair ? Lb : La;
+  if (pair) {
+    if (int rc = validate(Lb)) return rc;
+    if (La->index_kind != Lb->index_kind) { set_error("moments: index kinds differ (convert first)"); return BZ_E_INVALID; }
+    if (La->kept != Lb->kept) { set_error("moments: masks differ"); return BZ_E_INVALID; }
+  }
+  return launch_moments(make_geo(La), make_geo(lb), a_max, a_idx, pair ? b_max : a_max,
+                        pair ? b_idx : a_idx, pair, dc_only, record, ws, ws_bytes, S(stream));
+}
+
+int bz_round_to_kind(const void* in, int in_kind, void* out, int out_kind, int64_t n,
+                     int32_t* mismatch, void* stream) {
+  return launch_round_to_kind(in, in_kind, out, out_kind, n, mismatch, S(stream));
+}
+
+int bz_gradient(int ndim, const int64_t* shape, int kind, void* out, void* stream) {
+  if (ndim < 1 || ndim > BZ_MAX_DIMS) { set_error("gradient: bad ndim"); return BZ_E_INVALID; }
+  return launch_gradient(ndim, shape, kind, out, S(stream));
+}
+
+int bz_block(const bz_layout* L, const void* x, int x_kind, double* blocks, void* stream) {
+  if (int rc = validate(L)) return rc;
+  return launch_block(make_geo(L), x, x_kind, blocks, S(stream));
+}
+
+int bz_unblock(const bz_layout* L, const double* blocks, void* out, int out_kind, void* stream) {
+  if (int rc = validate(L)) return rc;
+  return launch_unblock(make_geo(L), blocks, out, out_kind, S(stream));
+}
+
+int bz_transform(const bz_layout* L, const double* in, double* out, int inverse, void* ws,
+                 size_t ws_bytes, void* stream) {
+  if (int rc = validate(L)) return rc;
+  if (int rc = need_matrices(L)) return rc;
+  return launch_transform(make_geo(L), in, out, inverse, ws, ws_bytes, S(stream));
+}
+
+int bz_bin(const bz_layout* L, const double* coeffs, void* maxima, void* full, void* stream) {
+  if (int rc = validate(L)) return rc;
+  return launch_bin(make_geo(L), coeffs, maxima, full, S(stream));
+}
+
+int bz_prune(const bz_layout* L, const void* full, void* flat, void* stream) {
+  if (int rc = validate(L)) return rc;
+  return launch_prune(make_geo(L), full, flat, S(stream));
+}
+
+int bz_unflatten(const bz_layout* L, const void* flat, void* full, void* stream) {
+  if (int rc = validate(L)) return rc;
+  return launch_unflatten(make_geo(L), flat, full, S(stream));
+}
+
+int bz_specified(const bz_layout* L, const void* maxima, const void* flat, double* out,
+                 void* stream) {
+  if (int rc = validate(L)) return rc;
+  return launch_specified(make_geo(L), maxima, flat, out, S(stream));
+}
+
+int bz_fill_random(void* out, int kind, int64_t n, int64_t offset, uint64_t seed, int dist,
+                   void* stream) {
+  return launch_fill_random(out, kind, n, offset, seed, dist, S(stream));
+}
+
+int bz_convert_indices(const void* in, int in_kind, void* out, int out_kind, int64_t n,
+                       void* stream) {
+  return launch_convert_indices(in, in_kind, out, out_kind, n, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,284 @@
+// bz_common.cuh -- shared device helpers for the B200 PyBlaz kernels.
+//
+// Kind traits, IEEE rounding into narrow float kinds (kinds.py:186-206),
+// exact and fast binning (codec.py:253-278), descriptor helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "../../include/bzc_b200.h"
+
+namespace bz {
+
+constexpr int kSMs = 148;  // B200
+
+// ------------------------------------------------------------------ errors --
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+// ------------------------------------------------------------- kind traits --
+template <int K> struct FloatKind;
+template <> struct FloatKind<BZ_BF16> { using T = uint16_t; static constexpr int SIG = 7,  EMIN = -126,  EMAX = 127; };
+template <> struct FloatKind<BZ_F16>  { using T = uint16_t; static constexpr int SIG = 10, EMIN = -14,   EMAX = 15; };
+template <> struct FloatKind<BZ_F32>  { using T = float;    static constexpr int SIG = 23, EMIN = -126,  EMAX = 127; };
+template <> struct FloatKind<BZ_F64>  { using T = double;   static constexpr int SIG = 52, EMIN = -1022, EMAX = 1023; };
+
+inline int float_kind_bytes(int k) { return k == BZ_F64 ? 8 : (k == BZ_F32 ? 4 : 2); }
+inline int index_kind_bytes(int k) { return 1 << k; }
+
+template <int K> struct IndexKind;
+template <> struct IndexKind<BZ_I8>  { using T = int8_t;  };
+template <> struct IndexKind<BZ_I16> { using T = int16_t; };
+template <> struct IndexKind<BZ_I32> { using T = int32_t; };
+template <> struct IndexKind<BZ_I64> { using T = int64_t; };
+
+// radius r = 2^(b-1)-1 as the reference's float(radius) (kinds.py:128-130; an
+// i64 radius rounds to 2^63).  clamp bound = largest f64 <= r (kinds.py:137-147).
+__host__ __device__ inline double radius_f64(int ik) {
+  switch (ik) {
+    case BZ_I8: return 127.0;
+    case BZ_I16: return 32767.0;
+    case BZ_I32: return 2147483647.0;
+    default: return 9223372036854775808.0;
+  }
+}
+__host__ __device__ inline double clamp_bound_f64(int ik) {
+  return ik == BZ_I64 ? 9223372036854774784.0 : radius_f64(ik);
+}
+
+__device__ __forceinline__ double pow2(int k) {  // exact 2^k, -1022 <= k <= 1023
+  return __hiloint2double((k + 1023) << 20, 0);
+}
+
+// IEEE round-to-nearest-even of a float64 into kind K, returned as float64.
+// Same algorithm as kinds.py:193-206: quantum 2^(max(e-1,emin)-sig),
+// rint(x/quantum)*quantum, overflow past max_finite -> signed inf.
+template <int K>
+__device__ __forceinline__ double round_to_kind(double x) {
+  if constexpr (K == BZ_F64) {
+    return x;
+  } else if constexpr (K == BZ_F32) {
+    return (double)__double2float_rn(x);  // cvt.rn.f32.f64 is IEEE RNE incl. subnormals/overflow
+  } else {
+    using FK = FloatKind<K>;
+    if (!isfinite(x) || x == 0.0) return x;
+    int e = ((__double2hiint(x) >> 20) & 0x7ff) - 1023;  // floor(log2|x|) for normal x
+    int q = (e > FK::EMIN ? e : FK::EMIN) - FK::SIG;
+    double r = rint(x * pow2(-q)) * pow2(q);
+    const double maxf = (2.0 - 1.0 / (double)(1 << FK::SIG)) * pow2(FK::EMAX);
+    if (fabs(r) > maxf) r = copysign(__longlong_as_double(0x7ff0000000000000ll), x);
+    return r;
+  }
+}
+
+__device__ __forceinline__ double round_to_kind_rt(double x, int k) {
+  switch (k) {
+    case BZ_BF16: return round_to_kind<BZ_BF16>(x);
+    case BZ_F16: return round_to_kind<BZ_F16>(x);
+    case BZ_F32: return round_to_kind<BZ_F32>(x);
+    default: return x;
+  }
+}
+
+// exact widening of stored values to f64
+__device__ __forceinline__ double widen(float v) { return (double)v; }
+__device__ __forceinline__ double widen(double v) { return v; }
+template <int K>
+__device__ __forceinline__ double load_kind(const void* p, int64_t i) {
+  if constexpr (K == BZ_F64) return reinterpret_cast<const double*>(p)[i];
+  else if constexpr (K == BZ_F32) return (double)reinterpret_cast<const float*>(p)[i];
+  else if constexpr (K == BZ_F16) {
+    __half h = __ushort_as_half(reinterpret_cast<const uint16_t*>(p)[i]);
+    return (double)__half2float(h);
+  } else {
+    uint32_t b = (uint32_t)reinterpret_cast<const uint16_t*>(p)[i] << 16;
+    return (double)__uint_as_float(b);
+  }
+}
+__device__ __forceinline__ double load_kind_rt(const void* p, int64_t i, int k) {
+  switch (k) {
+    case BZ_BF16: return load_kind<BZ_BF16>(p, i);
+    case BZ_F16: return load_kind<BZ_F16>(p, i);
+    case BZ_F32: return load_kind<BZ_F32>(p, i);
+    default: return load_kind<BZ_F64>(p, i);
+  }
+}
+// store a value ALREADY representable in kind K (exact narrowing)
+template <int K>
+__device__ __forceinline__ void store_kind(void* p, int64_t i, double v) {
+  if constexpr (K == BZ_F64) reinterpret_cast<double*>(p)[i] = v;
+  else if constexpr (K == BZ_F32) reinterpret_cast<float*>(p)[i] = (float)v;
+  else if constexpr (K == BZ_F16) reinterpret_cast<uint16_t*>(p)[i] = __half_as_ushort(__double2half(v));
+  else reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)(__float_as_uint((float)v) >> 16);
+}
+__device__ __forceinline__ void store_kind_rt(void* p, int64_t i, double v, int k) {
+  switch (k) {
+    case BZ_BF16: store_kind<BZ_BF16>(p, i, v); break;
+    case BZ_F16: store_kind<BZ_F16>(p, i, v); break;
+    case BZ_F32: store_kind<BZ_F32>(p, i, v); break;
+    default: store_kind<BZ_F64>(p, i, v); break;
+  }
+}
+
+__device__ __forceinline__ int64_t load_index_rt(const void* p, int64_t i, int ik) {
+  switch (ik) {
+    case BZ_I8: return reinterpret_cast<const int8_t*>(p)[i];
+    case BZ_I16: return reinterpret_cast<const int16_t*>(p)[i];
+    case BZ_I32: return reinterpret_cast<const int32_t*>(p)[i];
+    default: return reinterpret_cast<const int64_t*>(p)[i];
+  }
+}
+__device__ __forceinline__ void store_index_rt(void* p, int64_t i, int64_t v, int ik) {
+  switch (ik) {
+    case BZ_I8: reinterpret_cast<int8_t*>(p)[i] = (int8_t)v; break;
+    case BZ_I16: reinterpret_cast<int16_t*>(p)[i] = (int16_t)v; break;
+    case BZ_I32: reinterpret_cast<int32_t*>(p)[i] = (int32_t)v; break;
+    default: reinterpret_cast<int64_t*>(p)[i] = v; break;
+  }
+}
+
+// NaN-propagating max of |x| (np.max(np.abs(...)) semantics, codec.py:269)
+__device__ __forceinline__ double nanmax_abs(double m, double x) {
+  double a = fabs(x);
+  if (isnan(a) || isnan(m)) return __longlong_as_double(0x7ff8000000000000ll);
+  return a > m ? a : m;
+}
+
+// Exact reference binning of one coefficient (codec.py:272-278):
+// q = C / N (IEEE), non-finite -> 0, clip(rint(q * r), +-bound).
+__device__ __forceinline__ int64_t bin_exact(double c, double n, double r, double bound) {
+  double q = __ddiv_rn(c, n);
+  if (!isfinite(q)) q = 0.0;
+  double v = rint(__dmul_rn(q, r));
+  v = fmin(fmax(v, -bound), bound);
+  return (int64_t)v;
+}
+
+// Correctly rounded x / r for a constant divisor r using Markstein's
+// correction: q0 = x*y (y = RN(1/r)), e = x - q0*r exact by FMA,
+// q = RN(q0 + e*y).  Valid for finite x with |x| not in the subnormal
+// range (callers guarantee it per block; otherwise use __ddiv_rn).
+__device__ __forceinline__ double div_const(double x, double r, double y) {
+  double q0 = __dmul_rn(x, y);
+  double e = __fma_rn(-q0, r, x);
+  return __fma_rn(e, y, q0);
+}
+
+// Fast binning (see bz_fast_compress.cu): v = c * R, R = r / N, rounded once
+// to K-bit fixed point by an FMA against 1.5*2^(52-K); |v| <= r(1+2^-8) keeps
+// v*2^K inside the magic binade.  `near` flags fractions within W units of
+// one half, which the caller recomputes exactly with bin_exact.
+template <typename IT> struct FastBin;
+template <> struct FastBin<int8_t>  { static constexpr int K = 24; static constexpr int W = 1; using Fix = int32_t; };
+template <> struct FastBin<int16_t> { static constexpr int K = 15; static constexpr int W = 1; using Fix = int32_t; };
+template <> struct FastBin<int32_t> { static constexpr int K = 19; static constexpr int W = 2; using Fix = int64_t; };
+
+template <typename IT>
+__device__ __forceinline__ int fast_index(double c, double R, double rr, bool& near) {
+  using FB = FastBin<IT>;
+  constexpr double MAGIC = 1.5 * (double)(1ll << (52 - FB::K));
+  double t = __fma_rn(c, R, MAGIC);
+  typename FB::Fix fx;
+  if constexpr (sizeof(typename FB::Fix) == 4) {
+    fx = (int32_t)__double2loint(t);
+  } else {
+    fx = (int64_t)(__double_as_longlong(t) & ((1ll << 52) - 1)) - (1ll << 51);
+  }
+  constexpr typename FB::Fix HALF = (typename FB::Fix)1 << (FB::K - 1);
+  constexpr typename FB::Fix MASK = ((typename FB::Fix)1 << FB::K) - 1;
+  typename FB::Fix frac = fx & MASK;
+  near = near || ((frac - (HALF - FB::W)) >= 0 && (frac - (HALF - FB::W)) <= 2 * FB::W);
+  long long idx = (long long)((fx + HALF) >> FB::K);
+  long long ir = (long long)rr;
+  idx = idx > ir ? ir : (idx < -ir ? -ir : idx);
+  return (int)idx;
+}
+
+// ------------------------------------------------------------ descriptors --
+struct Geo {  // device-side copy of the layout geometry
+  int ndim;
+  int64_t shape[BZ_MAX_DIMS];
+  int32_t block[BZ_MAX_DIMS];
+  int64_t grid[BZ_MAX_DIMS];
+  int64_t stride[BZ_MAX_DIMS];   // dense element strides
+  int64_t nblocks;
+  int32_t bsize;                 // prod(block)
+  int32_t kept;
+  int32_t keeps_first;
+  int32_t float_kind, index_kind, transform;
+  const int32_t* kept_pos;
+  const int32_t* rank;
+  const double* matrices;
+  int32_t mat_off[BZ_MAX_DIMS];  // offset of axis a's matrix in `matrices`
+};
+
+inline Geo make_geo(const bz_layout* L) {
+  Geo g{};
+  g.ndim = L->ndim;
+  int64_t s = 1;
+  for (int a = L->ndim - 1; a >= 0; --a) { g.stride[a] = s; s *= L->shape[a]; }
+  g.nblocks = 1;
+  g.bsize = 1;
+  int off = 0;
+  for (int a = 0; a < L->ndim; ++a) {
+    g.shape[a] = L->shape[a];
+    g.block[a] = L->block[a];
+    g.grid[a] = L->grid[a];
+    g.nblocks *= L->grid[a];
+    g.bsize *= L->block[a];
+    g.mat_off[a] = off;
+    off += L->block[a] * L->block[a];
+  }
+  g.kept = L->kept;
+  g.keeps_first = L->keeps_first;
+  g.float_kind = L->float_kind;
+  g.index_kind = L->index_kind;
+  g.transform = L->transform;
+  g.kept_pos = L->kept_pos;
+  g.rank = L->rank;
+  g.matrices = L->matrices;
+  return g;
+}
+
+inline int64_t dense_count(const bz_layout* L) {
+  int64_t n = 1;
+  for (int a = 0; a < L->ndim; ++a) n *= L->shape[a];
+  return n;
+}
+inline int64_t block_count(const bz_layout* L) {
+  int64_t n = 1;
+  for (int a = 0; a < L->ndim; ++a) n *= L->grid[a];
+  return n;
+}
+inline int block_size(const bz_layout* L) {
+  int n = 1;
+  for (int a = 0; a < L->ndim; ++a) n *= L->block[a];
+  return n;
+}
+
+// dense offset of intrablock position `pos` (row-major) of block `b`, or -1 if padding
+__device__ __forceinline__ int64_t element_offset(const Geo& g, int64_t b, int pos) {
+  int64_t off = 0;
+  for (int a = g.ndim - 1; a >= 0; --a) {
+    int64_t gb = b % g.grid[a];
+    b /= g.grid[a];
+    int n = pos % g.block[a];
+    pos /= g.block[a];
+    int64_t c = gb * g.block[a] + n;
+    if (c >= g.shape[a]) return -1;
+    off += c * g.stride[a];
+  }
+  return off;
+}
+
+inline int grid_for(int64_t work, int threads, int per_sm = 8) {
+  int64_t b = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)kSMs * per_sm;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace bz

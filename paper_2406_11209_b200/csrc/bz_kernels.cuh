@@ -1,0 +1,53 @@
+// bz_kernels.cuh -- launcher declarations shared by the translation units.
+#pragma once
+#include <algorithm>
+
+#include "bz_common.cuh"
+
+namespace bz {
+
+// generic (bz_generic.cu)
+int launch_round_to_kind(const void* in, int in_kind, void* out, int out_kind, int64_t n,
+                         int32_t* mismatch, cudaStream_t s);
+int launch_convert_indices(const void* in, int in_kind, void* out, int out_kind, int64_t n,
+                           cudaStream_t s);
+int launch_gradient(int ndim, const int64_t* shape, int kind, void* out, cudaStream_t s);
+int launch_fill_random(void* out, int kind, int64_t n, int64_t offset, uint64_t seed, int dist,
+                       cudaStream_t s);
+int launch_block(const Geo& g, const void* x, int x_kind, double* blocks, cudaStream_t s);
+int launch_unblock(const Geo& g, const double* blocks, void* out, int out_kind, cudaStream_t s);
+int launch_transform(const Geo& g, const double* in, double* out, int inverse, void* ws,
+                     size_t ws_bytes, cudaStream_t s);
+int launch_bin(const Geo& g, const double* coeffs, void* maxima, void* full, cudaStream_t s);
+int launch_prune(const Geo& g, const void* full, void* flat, cudaStream_t s);
+int launch_unflatten(const Geo& g, const void* flat, void* full, cudaStream_t s);
+int launch_specified(const Geo& g, const void* maxima, const void* flat, double* out,
+                     cudaStream_t s);
+int launch_exact_compress(const Geo& g, const void* x, int x_kind, void* maxima, void* indices,
+                          const int32_t* list, const int32_t* count, int64_t max_blocks,
+                          void* ws, size_t ws_bytes, cudaStream_t s);
+size_t exact_compress_workspace(const Geo& g, int64_t max_blocks);
+int launch_exact_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
+                            int out_kind, void* ws, size_t ws_bytes, cudaStream_t s);
+
+// fused fast paths (bz_fast_*.cu)
+bool fast_supported(const Geo& g, int x_kind);
+int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices,
+                         int32_t* special_count, int32_t* special_list, cudaStream_t s);
+bool fast_decompress_supported(const Geo& g, int out_kind);
+int launch_fast_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
+                           int out_kind, cudaStream_t s);
+
+// compressed-domain ops (bz_ops.cu)
+int launch_negate(int ik, const void* in, void* out, int64_t n, cudaStream_t s);
+int launch_mul_scalar(const Geo& g, const void* maxima, const void* indices, double x,
+                      void* maxima_out, void* indices_out, cudaStream_t s);
+int launch_add(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
+               const void* b_max, const void* b_idx, int subtract, double shift, int mode,
+               void* out_max, void* out_idx, cudaStream_t s);
+size_t moments_workspace(const Geo& g);
+int launch_moments(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
+                   const void* b_max, const void* b_idx, int pair, int dc_only, double* record,
+                   void* ws, size_t ws_bytes, cudaStream_t s);
+
+}  // namespace bz

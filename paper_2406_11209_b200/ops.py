@@ -1,0 +1,374 @@
+"""Compressed-domain operations on the GPU (reference: pkg/src/bzc/ops.py).
+
+Same names, signatures, validation and exceptions as ops.py:58-348, plus
+``subtract`` (the reference composes it as add(a, negate(b)), cli.py:242).
+
+* negate / mul_scalar / add / subtract / add_scalar run one elementwise
+  kernel each and are bit-exact with the reference.
+* Every scalar reduction is computed from ONE fused pass (``bz_moments``)
+  that returns a partial record {n, DC means, centred DC co-moments, AC
+  sums}; the closed-form epilogue below (ops.py:239-348) turns it into the
+  reference's value.  Shards of a block-sharded array merge their records
+  (Chan's formulas) before the epilogue -- see ``distributed.py``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .codec import CompressedArray, workspace
+from .errors import (
+    MaskExcludesMeanCoefficient,
+    NegativeBaseWithFractionalWeight,
+    SettingsMismatch,
+    ZeroNormOperand,
+)
+
+__all__ = [
+    "SsimParams",
+    "negate",
+    "add",
+    "subtract",
+    "add_scalar",
+    "mul_scalar",
+    "dot",
+    "mean",
+    "covariance",
+    "variance",
+    "l2_norm",
+    "cosine_similarity",
+    "ssim",
+    "ssim_components",
+    "Record",
+    "moments_record",
+    "merge_records",
+]
+
+
+@dataclass(frozen=True)
+class SsimParams:
+    """SSIM stabilizers and weights (ops.py:58-83)."""
+
+    luminance_stabilizer: float = 1e-4
+    contrast_stabilizer: float = 9e-4
+    luminance_weight: float = 1.0
+    contrast_weight: float = 1.0
+    structure_weight: float = 1.0
+
+    def __post_init__(self):
+        if self.luminance_stabilizer < 0 or self.contrast_stabilizer < 0:
+            raise ValueError("stabilizers must be non-negative")
+
+    @classmethod
+    def for_data_range(cls, data_range: float, **weights) -> "SsimParams":
+        return cls(luminance_stabilizer=(0.01 * data_range) ** 2,
+                   contrast_stabilizer=(0.03 * data_range) ** 2, **weights)
+
+
+# ------------------------------------------------------------- validation --
+def _check_compatible(a: CompressedArray, b: CompressedArray, *, index_kind: bool = False):
+    """Same checks and message format as ops.py:100-116."""
+    problems = []
+    if a.original_shape != b.original_shape:
+        problems.append(f"shape {a.original_shape} vs {b.original_shape}")
+    sa, sb = a.settings, b.settings
+    if sa.block_shape != sb.block_shape:
+        problems.append(f"block shape {sa.block_shape} vs {sb.block_shape}")
+    if sa.mask != sb.mask:
+        problems.append("pruning masks differ")
+    if sa.transform is not sb.transform:
+        problems.append(f"transform {sa.transform.value} vs {sb.transform.value}")
+    if index_kind and sa.index_kind is not sb.index_kind:
+        problems.append(f"index kind {sa.index_kind.value} vs {sb.index_kind.value}")
+    if problems:
+        raise SettingsMismatch("; ".join(problems))
+
+
+def _require_first_coefficient(a: CompressedArray):
+    if not a.settings.mask.keeps_first:
+        raise MaskExcludesMeanCoefficient(
+            "operation needs the first (block-mean) coefficient, but the pruning mask drops it"
+        )
+
+
+def _stream(a: CompressedArray) -> int:
+    return _native.stream_handle(a.device)
+
+
+# ----------------------------------------------------------- elementwise ----
+def negate(a: CompressedArray) -> CompressedArray:
+    """{s, N, -F}; exact (ops.py:195-197).  Maxima are shared."""
+    out = torch.empty_like(a.indices)
+    _native.call("bz_negate", a.settings.index_kind.code, a.indices.data_ptr(), out.data_ptr(),
+                 a.indices.numel(), _stream(a))
+    return CompressedArray(a.original_shape, a.settings, a.maxima, out, _trusted=True)
+
+
+def _add(a: CompressedArray, b: CompressedArray, subtract: int) -> CompressedArray:
+    _check_compatible(a, b, index_kind=True)
+    out_max = torch.empty_like(a.maxima)
+    out_idx = torch.empty_like(a.indices)
+    La, Lb = a.layout(), b.layout()
+    bi = b.indices if b.device == a.device else b.indices.to(a.device)
+    bm = b.maxima if b.device == a.device else b.maxima.to(a.device)
+    _native.call("bz_add", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
+                 a.indices.data_ptr(), bm.data_ptr(), bi.data_ptr(), subtract,
+                 out_max.data_ptr(), out_idx.data_ptr(), _stream(a))
+    return CompressedArray(a.original_shape, a.settings, out_max, out_idx, _trusted=True)
+
+
+def add(a: CompressedArray, b: CompressedArray) -> CompressedArray:
+    """Elementwise sum with rebinning under a's kinds (ops.py:200-204); bit-exact."""
+    return _add(a, b, 0)
+
+
+def subtract(a: CompressedArray, b: CompressedArray) -> CompressedArray:
+    """a - b == add(a, negate(b)) bit for bit, in one pass."""
+    return _add(a, b, 1)
+
+
+def add_scalar(a: CompressedArray, x: float) -> CompressedArray:
+    """Shift each block's first coefficient by x*sqrt(prod i), rebin (ops.py:207-215)."""
+    _require_first_coefficient(a)
+    shift = float(x) * a.settings.block_mean_scale
+    out_max = torch.empty_like(a.maxima)
+    out_idx = torch.empty_like(a.indices)
+    L = a.layout()
+    _native.call("bz_add_scalar", ctypes.byref(L), a.maxima.data_ptr(), a.indices.data_ptr(),
+                 shift, out_max.data_ptr(), out_idx.data_ptr(), _stream(a))
+    return CompressedArray(a.original_shape, a.settings, out_max, out_idx, _trusted=True)
+
+
+def mul_scalar(a: CompressedArray, x: float) -> CompressedArray:
+    """N' = RN_kind(N*|x|), F' = F*sign(x) (ops.py:218-223).  x > 0 shares F."""
+    x = float(x)
+    out_max = torch.empty_like(a.maxima)
+    out_idx = None if x > 0 else torch.empty_like(a.indices)
+    L = a.layout()
+    _native.call("bz_mul_scalar", ctypes.byref(L), a.maxima.data_ptr(), a.indices.data_ptr(), x,
+                 out_max.data_ptr(), None if out_idx is None else out_idx.data_ptr(), _stream(a))
+    return CompressedArray(a.original_shape, a.settings, out_max,
+                           a.indices if out_idx is None else out_idx, _trusted=True)
+
+
+# ------------------------------------------------------------ reductions ----
+@dataclass(frozen=True)
+class Record:
+    """Partial sums of one array / shard (include/bzc_b200.h, bz_moments)."""
+
+    n: float
+    mean_a: float
+    mean_b: float
+    m_ab: float
+    m_aa: float
+    m_bb: float
+    s_ab: float
+    s_aa: float
+    s_bb: float
+
+    @classmethod
+    def from_array(cls, v) -> "Record":
+        v = [float(x) for x in np.asarray(v, dtype=np.float64).reshape(-1)[:9]]
+        return cls(*v)
+
+    def as_array(self) -> np.ndarray:
+        return np.array([self.n, self.mean_a, self.mean_b, self.m_ab, self.m_aa, self.m_bb,
+                         self.s_ab, self.s_aa, self.s_bb], dtype=np.float64)
+
+
+def merge_records(records) -> Record:
+    """Chan et al. pairwise merge, in the given (deterministic) order."""
+    acc = None
+    for r in records:
+        if acc is None or acc.n == 0.0:
+            acc = r
+            continue
+        if r.n == 0.0:
+            continue
+        n = acc.n + r.n
+        da, db = r.mean_a - acc.mean_a, r.mean_b - acc.mean_b
+        f = acc.n * r.n / n
+        acc = Record(
+            n,
+            acc.mean_a + da * (r.n / n),
+            acc.mean_b + db * (r.n / n),
+            acc.m_ab + r.m_ab + da * db * f,
+            acc.m_aa + r.m_aa + da * da * f,
+            acc.m_bb + r.m_bb + db * db * f,
+            acc.s_ab + r.s_ab,
+            acc.s_aa + r.s_aa,
+            acc.s_bb + r.s_bb,
+        )
+    return acc if acc is not None else Record(0, 0, 0, 0, 0, 0, 0, 0, 0)
+
+
+def moments_record(a: CompressedArray, b: CompressedArray | None = None, *,
+                   dc_only: bool = False) -> torch.Tensor:
+    """Launch the fused reduction; returns the device record (16 float64)."""
+    pair = b is not None and b is not a
+    dev = a.device
+    rec = torch.empty(_native.RECORD_DOUBLES, dtype=torch.float64, device=dev)
+    La = a.layout()
+    Lb = b.layout() if pair else La
+    bm = bi = None
+    if pair:
+        bm = b.maxima if b.device == dev else b.maxima.to(dev)
+        bi = b.indices if b.device == dev else b.indices.to(dev)
+        if b.settings.index_kind is not a.settings.index_kind:
+            # mixed index kinds are legal for reductions (ops.py:100-116): widen
+            wide = max(a.settings.index_kind, b.settings.index_kind, key=lambda k: k.bits)
+            if a.settings.index_kind is not wide:
+                return moments_record(b, a, dc_only=dc_only)[[0, 2, 1, 3, 5, 4, 6, 8, 7, 9, 10, 11, 12, 13, 14, 15]]
+            conv = torch.empty(bi.shape, dtype=wide.torch_dtype, device=dev)
+            _native.call("bz_convert_indices", bi.data_ptr(), b.settings.index_kind.code,
+                         conv.data_ptr(), wide.code, bi.numel(), _stream(a))
+            bi = conv
+            from .codec import layout as _layout
+
+            Lb = _layout(b.settings, b.original_shape, dev, index_kind=wide)
+    ws = workspace(_native.query("bz_moments_workspace", ctypes.byref(La)), dev)
+    _native.call("bz_moments", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
+                 a.indices.data_ptr(), bm.data_ptr() if pair else None,
+                 bi.data_ptr() if pair else None, int(pair), int(dc_only), rec.data_ptr(),
+                 ws.data_ptr(), ws.numel(), _stream(a))
+    return rec
+
+
+def _reduce(a, b=None, *, dc_only=False) -> Record:
+    """Record of the whole array (sharded arrays merge across ranks first)."""
+    hook = getattr(a, "_reduce_record", None)
+    if hook is not None:
+        return hook(b, dc_only)
+    return Record.from_array(moments_record(a, b, dc_only=dc_only).cpu().numpy())
+
+
+def _radius(a) -> float:
+    return float(a.settings.index_kind.radius)
+
+
+def _global_shape(a):
+    return getattr(a, "global_shape", a.original_shape)
+
+
+def _global_blocks(a) -> int:
+    return int(np.prod(a.settings.grid_for(_global_shape(a))))
+
+
+def _dot_from(rec: Record, keeps_first: bool) -> float:
+    dc = (rec.m_ab + rec.n * rec.mean_a * rec.mean_b) if keeps_first else 0.0
+    return rec.s_ab + dc
+
+
+def _sq_a(rec: Record, keeps_first: bool) -> float:
+    dc = (rec.m_aa + rec.n * rec.mean_a * rec.mean_a) if keeps_first else 0.0
+    return rec.s_aa + dc
+
+
+def _sq_b(rec: Record, keeps_first: bool) -> float:
+    dc = (rec.m_bb + rec.n * rec.mean_b * rec.mean_b) if keeps_first else 0.0
+    return rec.s_bb + dc
+
+
+def dot(a: CompressedArray, b: CompressedArray) -> float:
+    """Dot product of the underlying arrays (ops.py:226-241)."""
+    _check_compatible(a, b)
+    if a.settings.mask.kept_count == 0:
+        return 0.0
+    rec = _reduce(a, None if a is b else b)
+    return _dot_from(rec, a.settings.mask.keeps_first) / (_radius(a) * _radius(b))
+
+
+def l2_norm(a: CompressedArray) -> float:
+    """Euclidean norm sqrt(sum (F N)^2) / r (ops.py:291-297)."""
+    if a.settings.mask.kept_count == 0:
+        return 0.0
+    rec = _reduce(a)
+    return float(math.sqrt(max(_sq_a(rec, a.settings.mask.keeps_first), 0.0))) / _radius(a)
+
+
+def mean(a: CompressedArray, padding_corrected: bool = False) -> float:
+    """Mean from the first coefficients (ops.py:244-257)."""
+    _require_first_coefficient(a)
+    rec = _reduce(a, dc_only=True)
+    c = a.settings.block_mean_scale
+    firsts_mean = rec.mean_a / _radius(a)
+    if padding_corrected:
+        return float(c * (firsts_mean * rec.n) / np.prod(_global_shape(a)))
+    return float(firsts_mean / c)
+
+
+def _cov_from(rec_m: float, rec_s: float, a, b) -> float:
+    return (rec_m + rec_s) / (_radius(a) * _radius(b)) / (_global_blocks(a) * a.settings.block_size)
+
+
+def covariance(a: CompressedArray, b: CompressedArray) -> float:
+    """Population covariance over the padded count (ops.py:260-283)."""
+    _check_compatible(a, b)
+    _require_first_coefficient(a)
+    _require_first_coefficient(b)
+    rec = _reduce(a, None if a is b else b)
+    return _cov_from(rec.m_ab, rec.s_ab, a, b)
+
+
+def variance(a: CompressedArray) -> float:
+    """covariance(a, a) (ops.py:286-288)."""
+    return covariance(a, a)
+
+
+def cosine_similarity(a: CompressedArray, b: CompressedArray) -> float:
+    """dot / (|a| |b|); ZeroNormOperand on a zero norm (ops.py:300-306).  One pass."""
+    _check_compatible(a, b)
+    if a.settings.mask.kept_count == 0:
+        raise ZeroNormOperand("cosine similarity needs two nonzero operands")
+    kf = a.settings.mask.keeps_first
+    rec = _reduce(a, None if a is b else b)
+    na = math.sqrt(max(_sq_a(rec, kf), 0.0)) / _radius(a)
+    nb = math.sqrt(max(_sq_b(rec, kf), 0.0)) / _radius(b)
+    if na == 0.0 or nb == 0.0:
+        raise ZeroNormOperand("cosine similarity needs two nonzero operands")
+    return (_dot_from(rec, kf) / (_radius(a) * _radius(b))) / (na * nb)
+
+
+def _signed_power(base: float, weight: float, term: str) -> float:
+    if base < 0 and not float(weight).is_integer():
+        raise NegativeBaseWithFractionalWeight(
+            f"{term} term is negative ({base!r}) with non-integer weight {weight!r}"
+        )
+    return float(base) ** float(weight)
+
+
+def ssim_components(a: CompressedArray, b: CompressedArray,
+                    params: SsimParams | None = None) -> tuple[float, float, float]:
+    """Luminance, contrast, structure (ops.py:317-335), from one fused pass."""
+    params = params or SsimParams()
+    _check_compatible(a, b)
+    _require_first_coefficient(a)
+    _require_first_coefficient(b)
+    rec = _reduce(a, None if a is b else b)
+    c = a.settings.block_mean_scale
+    mu_a = (rec.mean_a / _radius(a)) / c
+    mu_b = (rec.mean_b / _radius(b)) / c
+    var_a = _cov_from(rec.m_aa, rec.s_aa, a, a)
+    var_b = _cov_from(rec.m_bb, rec.s_bb, b, b)
+    cov = _cov_from(rec.m_ab, rec.s_ab, a, b)
+    sd_a, sd_b = math.sqrt(max(var_a, 0.0)), math.sqrt(max(var_b, 0.0))
+    sl, sc = params.luminance_stabilizer, params.contrast_stabilizer
+    lum = (2 * mu_a * mu_b + sl) / (mu_a * mu_a + mu_b * mu_b + sl)
+    con = (2 * sd_a * sd_b + sc) / (var_a + var_b + sc)
+    st = (cov + sc / 2) / (sd_a * sd_b + sc / 2)
+    return float(lum), float(con), float(st)
+
+
+def ssim(a: CompressedArray, b: CompressedArray, params: SsimParams | None = None) -> float:
+    """Weighted product of the three terms (ops.py:338-348)."""
+    params = params or SsimParams()
+    lum, con, st = ssim_components(a, b, params)
+    return (_signed_power(lum, params.luminance_weight, "luminance")
+            * _signed_power(con, params.contrast_weight, "contrast")
+            * _signed_power(st, params.structure_weight, "structure"))

@@ -1,0 +1,156 @@
+"""GPU parity against the reference's own outputs (tests/golden, made by the real bzc).
+
+Contract: indices bit-exact except ties (tie = the
+reference's pre-rounding value within 2^-40 relative of a half integer);
+maxima bit-exact for BF16/F16/F32 kinds, <= 8 ulps for F64; decompress
+within 1e-13 * max|ref|; negate / add / subtract / add_scalar / mul_scalar
+bit-exact; reductions within 1e-9 relative (cosine / ssim 1e-9 absolute).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import bzc_oracle as o
+import golden_io
+
+pytestmark = pytest.mark.gpu
+
+CASES = golden_io.compress_cases()
+OPS = golden_io.op_cases()
+
+
+@pytest.fixture(scope="module")
+def bz():
+    import paper_2406_11209_b200 as m
+
+    assert torch.cuda.is_available()
+    return m
+
+
+def settings_of(bz, case):
+    mask = bz.PruningMask(tuple(case["block"]), case["mask"])
+    return bz.CodecSettings(tuple(case["block"]), bz.FloatKind(case["float_kind"]),
+                            bz.IndexKind(case["index_kind"]), bz.TransformFamily(case["transform"]),
+                            mask)
+
+
+def ref_compressed(bz, case):
+    s = settings_of(bz, case)
+    return bz.CompressedArray(tuple(case["input"].shape), s, case["maxima"], case["indices"])
+
+
+def check_maxima(got, ref, kind):
+    both_nan = np.isnan(got) & np.isnan(ref)
+    if kind == "f64":
+        ok = both_nan | (got == ref) | (golden_io.float_ulps(got, ref, "f64") <= 8)
+    else:
+        ok = both_nan | (got == ref)
+    assert np.all(ok), np.argwhere(~ok)[:5]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_compress_matches_reference(bz, case):
+    s = settings_of(bz, case)
+    a = bz.DenseArray(case["input"].shape, bz.FloatKind(case["input_kind"]), case["input"])
+    ca = bz.compress(a, s)
+    got_n = ca.maxima_f64().cpu().numpy()
+    check_maxima(got_n, case["maxima"], case["float_kind"])
+    got_i = ca.indices.cpu().numpy()
+    ref_i = case["indices"]
+    assert got_i.shape == ref_i.shape and got_i.dtype == ref_i.dtype
+    ties = o.prune_and_flatten(
+        o.tie_mask(case["coeffs"], case["maxima"], len(case["block"]), case["index_kind"]),
+        case["mask"])
+    bad = (got_i != ref_i) & ~ties
+    assert not bad.any(), f"{int(bad.sum())} non-tie index mismatches"
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_decompress_matches_reference(bz, case):
+    out = bz.decompress(ref_compressed(bz, case))
+    assert out.kind is bz.FloatKind.F64
+    got = out.numpy()
+    ref = case["decompressed"]
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    fin = np.isfinite(ref)
+    span = np.max(np.abs(ref[fin])) if fin.any() else 0.0
+    assert np.all(np.abs(got[fin] - ref[fin]) <= 1e-13 * span + 1e-300)
+
+
+@pytest.mark.parametrize("case", OPS, ids=[c["name"] for c in OPS])
+def test_ops_match_reference(bz, case):
+    ca = golden_io.compress_case(case["a"])
+    cb = golden_io.compress_case(case["b"])
+    a, b = ref_compressed(bz, ca), ref_compressed(bz, cb)
+    ref = case["arrays"]
+
+    def same(c, tag):
+        assert np.array_equal(c.maxima_f64().cpu().numpy(), ref[f"{tag}_max"], equal_nan=True), tag
+        assert np.array_equal(c.indices.cpu().numpy(), ref[f"{tag}_idx"]), tag
+
+    assert np.array_equal(bz.negate(a).indices.cpu().numpy(), ref["negate_idx"])
+    same(bz.add(a, b), "add")
+    same(bz.subtract(a, b), "sub")
+    same(bz.add(a, bz.negate(b)), "sub")
+    same(bz.add(a, a), "addself")
+    for j, x in enumerate(case["scalars"]):
+        same(bz.mul_scalar(a, x), f"mul{j}")
+    if "addscalar_max" in ref:
+        same(bz.add_scalar(a, 0.75), "addscalar")
+    res = case["results"]
+    got = {
+        "dot": bz.dot(a, b), "dot_self": bz.dot(a, a), "l2_a": bz.l2_norm(a),
+        "l2_b": bz.l2_norm(b), "cos": bz.cosine_similarity(a, b),
+    }
+    if "mean_a" in res:
+        lum, con, st = bz.ssim_components(a, b)
+        got.update({
+            "mean_a": bz.mean(a), "mean_a_pc": bz.mean(a, padding_corrected=True),
+            "cov": bz.covariance(a, b), "var_a": bz.variance(a), "var_b": bz.variance(b),
+            "ssim_l": lum, "ssim_c": con, "ssim_s": st, "ssim": bz.ssim(a, b),
+            "ssim_self": bz.ssim(a, a),
+        })
+    for k, v in got.items():
+        assert math.isclose(v, res[k], rel_tol=1e-9, abs_tol=1e-12), (k, v, res[k])
+
+
+@pytest.mark.parametrize("kind", ["bf16", "f16", "f32", "f64"])
+def test_round_to_kind_bit_exact(bz, kind):
+    arrays, _ = golden_io.load()
+    got = bz.kinds.round_to_kind(arrays["k/input"], bz.FloatKind(kind)).cpu().numpy()
+    ref = arrays[f"k/{kind}"]
+    assert np.array_equal(got, ref, equal_nan=True)
+    assert np.array_equal(np.signbit(got), np.signbit(ref))
+
+
+def test_gradient_bit_exact(bz):
+    arrays, _ = golden_io.load()
+    got = bz.gradient_array((5, 7, 3)).numpy()
+    assert np.array_equal(got, arrays["g/gradient_5x7x3"])
+
+
+def test_reference_known_answers(bz):
+    """test_codec.py:45-63, 132-146, 165-172 known answers."""
+    s = bz.CodecSettings((8, 8), bz.FloatKind.F64, bz.IndexKind.I16)
+    ca = bz.compress(bz.DenseArray.of(np.full((8, 8), 5.0)), s)
+    n = float(ca.maxima_f64().cpu()[0, 0])
+    assert n == pytest.approx(40.0, rel=1e-13)
+    flat = ca.indices.cpu().numpy().ravel()
+    assert flat[0] == 32767 and not flat[1:].any()
+    z = bz.compress(bz.DenseArray.of(np.zeros((8, 8))), bz.CodecSettings((4, 4), bz.FloatKind.F64))
+    assert not z.maxima_f64().cpu().numpy().any() and not z.indices.cpu().numpy().any()
+    # binning goldens through the building block
+    c = bz.BlockedArray((1,), (4,), (4,), bz.FloatKind.F64, np.array([[16.0, 0.0, 0.0, 0.0]]))
+    m, idx = bz.bin_coefficients(c, bz.IndexKind.I8)
+    assert float(m.cpu()[0]) == 16.0 and idx.cpu().numpy().tolist() == [[127, 0, 0, 0]]
+    c = bz.BlockedArray((1,), (2,), (2,), bz.FloatKind.F64, np.array([[1.0, 0.5]]))
+    _, idx = bz.bin_coefficients(c, bz.IndexKind.I8)
+    assert idx.cpu().numpy().tolist() == [[127, 64]]  # 63.5 -> 64 (ties to even)
+    # +-r reconstructs exactly +-N
+    s4 = bz.CodecSettings((4,), bz.FloatKind.F64, bz.IndexKind.I8)
+    ca = bz.CompressedArray((4,), s4, np.array([16.0]), np.array([[127, 0, 0, 0]], dtype=np.int8))
+    chat = bz.specified_coefficients(ca).blocks.cpu().numpy()
+    assert np.array_equal(chat, [[16.0, 0.0, 0.0, 0.0]])

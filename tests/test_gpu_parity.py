@@ -1,0 +1,279 @@
+"""GPU path vs the CPU oracle on seeded inputs, plus size-independent properties
+at the BASELINE.json sizes.  All calls go through the public API, which calls
+the sm_100a library (include/bzc_b200.h) via ctypes."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import bzc_oracle as o
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bz():
+    import paper_2406_11209_b200 as m
+
+    assert torch.cuda.is_available()
+    return m
+
+
+def _settings(bz, block, fk, ik, fam="dct", mask_bits=None):
+    mask = None if mask_bits is None else bz.PruningMask(tuple(block), mask_bits)
+    return bz.CodecSettings(tuple(block), bz.FloatKind(fk), bz.IndexKind(ik),
+                            bz.TransformFamily(fam), mask)
+
+
+def _lowpass(block, k):
+    return np.indices(block).sum(axis=0) <= k
+
+
+def parity(bz, x, block, fk, ik, fam="dct", mask_bits=None, report=None):
+    """compress + decompress + ops vs oracle; returns the tie fraction."""
+    s = _settings(bz, block, fk, ik, fam, mask_bits)
+    os_ = o.Settings(block, fk, ik, fam, mask_bits)
+    ca = bz.compress(bz.DenseArray.of(x, bz.FloatKind(fk)), s)
+    x64 = o.round_to_kind(x, fk)
+    ref = o.compress(x64, os_)
+    coeffs = o.coefficients(x64, os_)
+    got_n = ca.maxima_f64().cpu().numpy()
+    if fk == "f64":
+        assert np.all((got_n == ref.maxima) | (np.abs(got_n - ref.maxima) <= 8 * np.spacing(ref.maxima)))
+    else:
+        assert np.array_equal(got_n, ref.maxima)
+    got_i = ca.indices.cpu().numpy()
+    ties = o.prune_and_flatten(o.tie_mask(coeffs, ref.maxima, len(block), ik), os_.mask_bits)
+    diff = got_i != ref.indices
+    assert not (diff & ~ties).any(), int((diff & ~ties).sum())
+    # decompress of the REFERENCE's compressed data isolates the decompress kernel
+    rc = bz.CompressedArray(x.shape, s, ref.maxima, ref.indices)
+    dec = bz.decompress(rc).numpy()
+    want = o.decompress(ref)
+    span = np.max(np.abs(want))
+    assert np.max(np.abs(dec - want)) <= 1e-13 * span
+    frac = diff.sum() / max(diff.size, 1)
+    if report is not None:
+        report.append(frac)
+    return ca, ref, frac
+
+
+@pytest.mark.parametrize("shape,block,fk,ik", [
+    ((256, 256, 256), (8, 8, 8), "f32", "i8"),      # C1 at full size
+    ((512, 512), (4, 4), "f64", "i16"),              # C2 slab
+    ((32, 32, 32, 16), (4, 4, 4, 4), "f32", "i8"),   # C5 slab, full mask
+    ((100, 70), (8, 8), "f64", "i16"),
+    ((1000,), (8,), "f32", "i16"),
+    ((333,), (4,), "f64", "i32"),
+    ((40, 33, 20), (4, 4, 4), "f32", "i16"),
+])
+def test_compress_parity_dct(bz, shape, block, fk, ik):
+    rng = np.random.default_rng(hash((shape, block)) % 2**32)
+    x = rng.normal(size=shape)
+    _, _, frac = parity(bz, x, block, fk, ik)
+    print(f"tie fraction {shape} {block}: {frac:.3e}")
+
+
+@pytest.mark.parametrize("shape,block,fk,ik", [
+    ((64, 64, 64), (8, 8, 8), "f32", "i8"),
+    ((96, 64), (4, 4), "f64", "i16"),
+    ((16, 16, 16, 16), (4, 4, 4, 4), "f32", "i8"),
+])
+def test_compress_parity_haar(bz, shape, block, fk, ik):
+    x = np.random.default_rng(7).uniform(-2, 2, size=shape)
+    parity(bz, x, block, fk, ik, fam="haar")
+
+
+def test_compress_parity_c5_lowpass(bz):
+    shape = (32, 32, 32, 16)
+    x = o.gradient_array(shape) + 0.01 * np.random.default_rng(7).normal(size=shape)
+    ca, ref, _ = parity(bz, x, (4, 4, 4, 4), "f32", "i8", mask_bits=_lowpass((4, 4, 4, 4), 4))
+    assert ca.indices.shape[-1] == 66
+
+
+@pytest.mark.parametrize("fk", ["bf16", "f16"])
+def test_compress_parity_narrow_kinds(bz, fk):
+    x = np.random.default_rng(3).normal(size=(64, 64, 8))
+    parity(bz, x, (8, 8, 8), fk, "i16")
+
+
+def test_generic_block_shapes(bz):
+    rng = np.random.default_rng(11)
+    for shape, block in [((12, 9, 16), (4, 2, 8)), ((4, 3, 4, 2, 5), (2, 2, 2, 2, 4)),
+                         ((40, 40), (32, 32)), ((9, 7), (1, 1)), ((17,), (2,))]:
+        parity(bz, rng.normal(size=shape), block, "f64", "i16")
+
+
+@pytest.mark.parametrize("shape,block,fk,ik", [
+    ((64, 64, 64), (8, 8, 8), "f32", "i8"),
+    ((256, 128), (4, 4), "f64", "i16"),
+    ((16, 16, 16, 16), (4, 4, 4, 4), "f32", "i8"),
+    ((96, 64), (8, 8), "f32", "i32"),
+])
+def test_fast_and_generic_agree(bz, monkeypatch, shape, block, fk, ik):
+    """Fused kernel vs the exact generic kernel on the same data."""
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=shape)
+    s = _settings(bz, block, fk, ik)
+    assert bz.is_fast_path(s, shape)
+    a = bz.DenseArray.of(x, bz.FloatKind(fk))
+    fast = bz.compress(a, s)
+    fast_dec = bz.decompress(fast).values
+    monkeypatch.setenv("BZC_B200_FORCE_GENERIC", "1")
+    generic = bz.compress(a, s)
+    gen_dec = bz.decompress(fast).values
+    monkeypatch.delenv("BZC_B200_FORCE_GENERIC")
+    if fk == "f64":
+        rel = ((fast.maxima - generic.maxima).abs() / generic.maxima.abs().clamp_min(1e-300)).max().item()
+        assert rel <= 1e-15
+    else:
+        assert torch.equal(fast.maxima, generic.maxima)
+    d = (fast.indices != generic.indices).double().mean().item()
+    assert d < 1e-5
+    assert ((fast_dec - gen_dec).abs().max() <= 1e-13 * gen_dec.abs().max()).item()
+
+
+# ------------------------------------------------------------- building blocks --
+def test_block_unblock_transform_bin(bz):
+    rng = np.random.default_rng(1)
+    x = rng.normal(size=(19, 13, 10))
+    a = bz.DenseArray.of(x)
+    b = bz.block(a, (8, 4, 2))
+    assert np.array_equal(b.blocks.cpu().numpy(), o.block(x, (8, 4, 2)))
+    assert np.array_equal(bz.unblock(b).numpy(), x)
+    mats = bz.transforms_for((8, 4, 2), bz.TransformFamily.DCT) if hasattr(bz, "transforms_for") else \
+        [bz.make_transform(i, bz.TransformFamily.DCT) for i in (8, 4, 2)]
+    c = bz.forward_transform(b, mats)
+    want = o.forward_transform(o.block(x, (8, 4, 2)), [m.entries for m in mats])
+    assert np.allclose(c.blocks.cpu().numpy(), want, rtol=0, atol=1e-13)
+    back = bz.inverse_transform(c, mats)
+    assert np.allclose(back.blocks.cpu().numpy(), o.block(x, (8, 4, 2)), atol=1e-13)
+    m, idx = bz.bin_coefficients(c, bz.IndexKind.I16, bz.FloatKind.F32)
+    rm, ri = o.bin_coefficients(c.blocks.cpu().numpy(), 3, "i16", "f32")
+    assert np.array_equal(bz.kinds.widen(m).cpu().numpy(), rm)
+    assert np.array_equal(idx.cpu().numpy(), ri)  # same coefficients -> bit-exact
+    mask = bz.PruningMask((8, 4, 2), rng.uniform(size=(8, 4, 2)) < 0.4)
+    flat = bz.prune_and_flatten(idx, mask)
+    assert np.array_equal(flat.cpu().numpy(), o.prune_and_flatten(ri, mask.bits))
+    full = bz.unflatten(flat, mask)
+    assert np.array_equal(full.cpu().numpy(), o.unflatten(flat.cpu().numpy(), mask.bits))
+
+
+def test_specified_coefficients_exact(bz):
+    rng = np.random.default_rng(2)
+    x = rng.normal(size=(32, 32))
+    s = _settings(bz, (4, 4), "f32", "i16")
+    ca = bz.compress(bz.DenseArray.of(x, bz.FloatKind.F32), s)
+    ref = o.Compressed(x.shape, o.Settings((4, 4), "f32", "i16"), ca.maxima_f64().cpu().numpy(),
+                       ca.indices.cpu().numpy())
+    assert np.array_equal(bz.specified_coefficients(ca).blocks.cpu().numpy(),
+                          o.specified_coefficients(ref))
+
+
+# --------------------------------------------------------------- operators --
+@pytest.mark.parametrize("shape,block,fk,ik,mask", [
+    ((128, 128, 128), (8, 8, 8), "f32", "i8", None),
+    ((1024, 1024), (4, 4), "f64", "i16", None),
+    ((32, 32, 32, 16), (4, 4, 4, 4), "f32", "i8", "lowpass"),
+    ((50, 37, 21), (8, 8, 8), "f32", "i8", None),
+])
+def test_ops_parity(bz, shape, block, fk, ik, mask):
+    rng = np.random.default_rng(9)
+    bits = _lowpass(block, 4) if mask == "lowpass" else None
+    s = _settings(bz, block, fk, ik, mask_bits=bits)
+    os_ = o.Settings(block, fk, ik, "dct", bits)
+    xa = rng.uniform(0, 1, size=shape)
+    xb = 0.5 * xa + 0.5 * rng.uniform(0, 1, size=shape)
+    ra, rb = o.compress(o.round_to_kind(xa, fk), os_), o.compress(o.round_to_kind(xb, fk), os_)
+    a = bz.CompressedArray(shape, s, ra.maxima, ra.indices)
+    b = bz.CompressedArray(shape, s, rb.maxima, rb.indices)
+    # bit-exact elementwise ops
+    for got, want in ((bz.add(a, b), o.add(ra, rb)), (bz.subtract(a, b), o.subtract(ra, rb)),
+                      (bz.mul_scalar(a, -0.37), o.mul_scalar(ra, -0.37)),
+                      (bz.add_scalar(a, 0.25), o.add_scalar(ra, 0.25)),
+                      (bz.negate(a), o.negate(ra))):
+        assert np.array_equal(got.maxima_f64().cpu().numpy(), want.maxima)
+        assert np.array_equal(got.indices.cpu().numpy(), want.indices)
+    # reductions
+    pairs = {
+        "dot": (bz.dot(a, b), o.dot(ra, rb)),
+        "l2": (bz.l2_norm(a), o.l2_norm(ra)),
+        "mean": (bz.mean(a), o.mean(ra)),
+        "mean_pc": (bz.mean(a, True), o.mean(ra, True)),
+        "var": (bz.variance(a), o.variance(ra)),
+        "cov": (bz.covariance(a, b), o.covariance(ra, rb)),
+        "cos": (bz.cosine_similarity(a, b), o.cosine_similarity(ra, rb)),
+        "ssim": (bz.ssim(a, b), o.ssim(ra, rb)),
+    }
+    for k, (g, w) in pairs.items():
+        assert math.isclose(g, w, rel_tol=1e-9, abs_tol=1e-12), (k, g, w)
+
+
+def test_mixed_index_kinds_reduction(bz):
+    rng = np.random.default_rng(4)
+    x, y = rng.normal(size=(64, 64)), rng.normal(size=(64, 64))
+    s8 = _settings(bz, (8, 8), "f32", "i8")
+    s16 = _settings(bz, (8, 8), "f64", "i16")
+    a = bz.compress(bz.DenseArray.of(x, bz.FloatKind.F32), s8)
+    b = bz.compress(bz.DenseArray.of(y, bz.FloatKind.F64), s16)
+    ra = o.Compressed(x.shape, o.Settings((8, 8), "f32", "i8"), a.maxima_f64().cpu().numpy(), a.indices.cpu().numpy())
+    rb = o.Compressed(y.shape, o.Settings((8, 8), "f64", "i16"), b.maxima_f64().cpu().numpy(), b.indices.cpu().numpy())
+    assert math.isclose(bz.dot(a, b), o.dot(ra, rb), rel_tol=1e-9)
+    assert math.isclose(bz.dot(b, a), o.dot(rb, ra), rel_tol=1e-9)
+    assert math.isclose(bz.covariance(a, b), o.covariance(ra, rb), rel_tol=1e-9, abs_tol=1e-15)
+
+
+# ------------------------------------------- full-size properties (BASELINE sizes) --
+def _fill(bz, shape, kind, seed, dist=0):
+    from paper_2406_11209_b200 import _native
+
+    t = torch.empty(shape, dtype=kind.torch_dtype, device="cuda")
+    _native.call("bz_fill_random", t.data_ptr(), kind.code, t.numel(), 0, seed, dist,
+                 _native.stream_handle())
+    return bz.DenseArray.wrap(t, kind)
+
+
+def test_c2_full_size_properties(bz):
+    """8192^2 f64, 4x4, I16: round-trip error bound, l2 vs dense norm, negate identity."""
+    a = _fill(bz, (8192, 8192), bz.FloatKind.F64, 2)
+    s = _settings(bz, (4, 4), "f64", "i16")
+    ca = bz.compress(a, s)
+    out = bz.decompress(ca).values
+    err = (out - a.values).abs().reshape(2048, 4, 2048, 4).amax(dim=(1, 3))
+    nmax = ca.maxima_f64()
+    # per-block bound: sum over coefficients of N/(2r) * max|H| <= N/(2r) * 16
+    assert bool((err <= nmax / (2 * 32767) * 16 * (1 + 1e-9)).all())
+    l2 = bz.l2_norm(ca)
+    dense = float(torch.linalg.vector_norm(out).item())
+    assert math.isclose(l2, dense, rel_tol=1e-9)
+    assert bz.negate(bz.negate(ca)) == ca
+    z = bz.decompress(bz.add(ca, bz.negate(ca))).values
+    assert int(torch.count_nonzero(z).item()) == 0
+
+
+def test_c3_full_size_chain(bz):
+    """1024^3 f32, 8^3, I8: mul_scalar(add(a,b), .5) then mean / variance vs dense."""
+    s = _settings(bz, (8, 8, 8), "f32", "i8")
+    a = bz.compress(_fill(bz, (1024, 1024, 1024), bz.FloatKind.F32, 3), s)
+    b = bz.compress(_fill(bz, (1024, 1024, 1024), bz.FloatKind.F32, 4), s)
+    t = bz.mul_scalar(bz.add(a, b), 0.5)
+    m, v = bz.mean(t), bz.variance(t)
+    dense = bz.decompress(t, bz.FloatKind.F32).values
+    dm = float(dense.double().mean().item())
+    dv = float(dense.double().var(unbiased=False).item())
+    assert abs(m - dm) <= 1e-6 * max(1.0, abs(dm))
+    assert math.isclose(v, dv, rel_tol=1e-5)
+    assert math.isclose(bz.l2_norm(a) ** 2, bz.dot(a, a), rel_tol=1e-9)
+
+
+def test_partition_invariance_of_random_fill(bz):
+    from paper_2406_11209_b200 import _native
+
+    full = torch.empty(1 << 20, dtype=torch.float32, device="cuda")
+    part = torch.empty(1 << 19, dtype=torch.float32, device="cuda")
+    s = _native.stream_handle()
+    _native.call("bz_fill_random", full.data_ptr(), 2, full.numel(), 0, 9, 0, s)
+    _native.call("bz_fill_random", part.data_ptr(), 2, part.numel(), 1 << 19, 9, 0, s)
+    assert torch.equal(full[1 << 19:], part)
