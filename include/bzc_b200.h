@@ -57,6 +57,8 @@ enum {
  *   rank[prod(block)] position -> rank in kept_pos, -1 if pruned
  *   matrices          per-axis transform entries [sample][basis], axis 0 first,
  *                     each block[a]*block[a] doubles (transforms.py:67-98)
+ *   matrices_host     the same entries in host memory (optional; the fused
+ *                     kernels carry them as kernel parameters)
  */
 typedef struct bz_layout {
   int32_t ndim;
@@ -71,6 +73,7 @@ typedef struct bz_layout {
   const int32_t* kept_pos;
   const int32_t* rank;
   const double* matrices;
+  const double* matrices_host;
 } bz_layout;
 
 /* Library identification / diagnostics. */

@@ -46,6 +46,7 @@ class Layout(ctypes.Structure):
         ("kept_pos", ctypes.c_void_p),
         ("rank", ctypes.c_void_p),
         ("matrices", ctypes.c_void_p),
+        ("matrices_host", ctypes.c_void_p),
     ]
 
 

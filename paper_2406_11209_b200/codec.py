@@ -185,10 +185,13 @@ def _tables(settings: CodecSettings, device: torch.device):
                 kept = settings.mask.flat_kept.astype(np.int32)
                 rank = np.full(settings.block_size, -1, dtype=np.int32)
                 rank[kept] = np.arange(kept.size, dtype=np.int32)
+                host = np.ascontiguousarray(
+                    np.concatenate([m.entries.reshape(-1) for m in settings.matrices()]))
                 t = (
                     torch.from_numpy(kept if kept.size else np.zeros(1, np.int32)).to(device),
                     torch.from_numpy(rank).to(device),
                     matrices_tensor(settings.matrices(), device),
+                    host,
                 )
                 _TABLES[key] = t
     return t
@@ -197,7 +200,7 @@ def _tables(settings: CodecSettings, device: torch.device):
 def layout(settings: CodecSettings, shape, device: torch.device, *,
            index_kind: IndexKind | None = None) -> _native.Layout:
     """The C-ABI descriptor of an array of `shape` compressed with `settings`."""
-    kept_pos, rank, mats = _tables(settings, device)
+    kept_pos, rank, mats, host = _tables(settings, device)
     L = _native.Layout()
     L.ndim = settings.ndim
     L.float_kind = settings.float_kind.code
@@ -212,6 +215,7 @@ def layout(settings: CodecSettings, shape, device: torch.device, *,
     L.kept_pos = kept_pos.data_ptr()
     L.rank = rank.data_ptr()
     L.matrices = mats.data_ptr()
+    L.matrices_host = host.ctypes.data
     return L
 
 

@@ -211,6 +211,7 @@ struct Geo {  // device-side copy of the layout geometry
   const int32_t* kept_pos;
   const int32_t* rank;
   const double* matrices;
+  const double* matrices_host;
   int32_t mat_off[BZ_MAX_DIMS];  // offset of axis a's matrix in `matrices`
 };
 
@@ -239,6 +240,7 @@ inline Geo make_geo(const bz_layout* L) {
   g.kept_pos = L->kept_pos;
   g.rank = L->rank;
   g.matrices = L->matrices;
+  g.matrices_host = L->matrices_host;
   return g;
 }
 

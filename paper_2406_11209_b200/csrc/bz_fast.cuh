@@ -1,20 +1,31 @@
 // bz_fast.cuh -- shared pieces of the fused compress / decompress kernels.
 //
-// Work decomposition ("register planes"), for a block of E^D elements:
-//   * D <= 2: one thread owns a whole block (E or E*E values in registers).
-//   * D = 3, 4: TB = E^(D-2) threads own one block; thread o holds the E x E
-//     plane of the two fastest axes at outer position o.  The fast-axis and
-//     row transforms run in registers; one shared-memory exchange hands each
-//     thread all outer positions of E*E/TB plane coefficients, and the outer
-//     transform runs in registers again.  No f64 value touches shared memory
-//     more than once per direction.
-// Threads are laid out outer-major (t = o * BPC + lb), so consecutive lanes
-// hold consecutive blocks along the fastest grid axis and every global row
-// access is a run of contiguous 16-byte vectors.
+// Bit-exact transform.  The reference's np.tensordot (OpenBLAS dgemm, kernel
+// sizes <= 32) evaluates every coefficient as a sequential FMA chain
+// acc = fma(x[n], H[n][k], acc), n ascending from acc = +0, one axis at a
+// time, axis 0 first (transforms.py:118-126).  We evaluate exactly that chain,
+// with the reference's own matrix entries carried as kernel parameters (DFMA
+// constant-bank operands), so coefficients -- hence maxima, indices and
+// decompressed values -- are bit-identical to the reference, not merely
+// within a tolerance.  (Verified on every golden case, tests/golden.)
+//
+// Work decomposition for a block of E^D elements ("slices"):
+//   a thread owns an E x E slice of two block axes (P, Q) at fixed
+//   coordinates of the other D-2 axes; TB = E^(D-2) threads own a block.
+//   Transforms along P or Q run in registers.  To reach another axis the
+//   TB threads of a block exchange through shared memory in the block's
+//   canonical (row-major) layout, XOR-swizzled by the block's slot so that
+//   lanes of a warp (consecutive blocks) hit distinct banks.
+//   D=2: one thread per block, slice (0,1).
+//   D=3: load slice (0,2) | axis 0 | exchange -> (1,2) | axes 1, 2.
+//   D=4: load slice (0,3) | axis 0 | exchange -> (1,2) | axes 1, 2 |
+//        exchange -> (2,3) | axis 3.
+// Threads are laid out t = o * BPC + lb (o = slice within block, lb = block
+// slot), so consecutive lanes own consecutive blocks along the fastest grid
+// axis and every dense row access is a run of contiguous 16-byte vectors.
 #pragma once
 
 #include "bz_common.cuh"
-#include "bz_transforms.cuh"
 
 namespace bz {
 
@@ -24,7 +35,6 @@ template <int D, int E>
 struct Tile {
   static constexpr int TB = D >= 3 ? ipow(E, D - 2) : 1;  // threads per block
   static constexpr int NIN = D >= 2 ? E * E : E;          // values per thread
-  static constexpr int M = NIN / TB;                      // plane positions per thread after exchange
   static constexpr int BS = ipow(E, D);                   // block size
   static constexpr int NT = NIN >= 64 ? 128 : 256;        // threads per CTA
   static constexpr int BPC = NT / TB;                     // blocks per CTA tile
@@ -39,13 +49,19 @@ struct FastGeo {
   int64_t ntiles;
   int32_t kept;
   int32_t full_mask;
-  int32_t vec_in;    // 16-byte vector access legal on the dense side
+  int32_t vec_dense;  // 16-byte vector access legal on the dense side
   const int32_t* rank;
-  const int32_t* kept_pos;
 };
 
-inline FastGeo make_fast_geo(const Geo& g, int bpc, const void* dense, int dense_bytes) {
-  FastGeo f{};
+struct FastParams {
+  FastGeo f;
+  double H[64];  // reference matrix entries [sample][basis] (E <= 8)
+};
+
+inline bool make_fast_params(const Geo& g, int bpc, const void* dense, int dense_bytes,
+                             FastParams& p) {
+  FastGeo& f = p.f;
+  f = FastGeo{};
   for (int a = 0; a < g.ndim; ++a) {
     f.shape[a] = g.shape[a];
     f.grid[a] = g.grid[a];
@@ -56,51 +72,135 @@ inline FastGeo make_fast_geo(const Geo& g, int bpc, const void* dense, int dense
   f.kept = g.kept;
   f.full_mask = g.kept == g.bsize;
   f.rank = g.rank;
-  f.kept_pos = g.kept_pos;
-  int E = g.block[g.ndim - 1];
+  const int E = g.block[g.ndim - 1];
   bool ok = ((uintptr_t)dense % 16 == 0) && ((E * dense_bytes) % 16 == 0);
-  if (g.ndim >= 2) ok = ok && ((g.stride[g.ndim - 2] * dense_bytes) % 16 == 0);
-  f.vec_in = ok;
-  return f;
+  for (int a = 0; a + 1 < g.ndim; ++a) ok = ok && ((g.stride[a] * dense_bytes) % 16 == 0);
+  f.vec_dense = ok;
+  if (!g.matrices_host) return false;
+  for (int i = 0; i < E * E; ++i) p.H[i] = g.matrices_host[i];  // every axis uses the same E
+  return true;
 }
 
-// decode block id -> block coordinates; returns the dense offset of the
-// thread's plane origin (outer intra coords from o) and whether the plane
-// lies fully inside the array.  `plane_valid` = false when the outer intra
-// coordinate itself is padding (the plane is all zeros).
+// ------------------------------------------------------------------ slices --
 template <int D, int E>
-__device__ __forceinline__ void plane_origin(const FastGeo& f, int64_t b, int o, int64_t& off,
-                                             bool& interior, bool& plane_valid,
-                                             int64_t (&gc)[4]) {
-  int64_t rem = b;
+__host__ __device__ constexpr int axis_stride(int a) { return ipow(E, D - 1 - a); }
+
+// canonical position of slice element (0,0) for slice axes (P,Q) at fixed
+// coordinates o (row-major over the other axes in ascending order)
+template <int D, int E, int P, int Q>
+__device__ __forceinline__ int slice_base(int o) {
+  int pos = 0;
 #pragma unroll
   for (int a = D - 1; a >= 0; --a) {
-    gc[a] = rem % f.grid[a];
-    rem /= f.grid[a];
-  }
-  off = 0;
-  interior = true;
-  plane_valid = true;
-  // outer axes 0..D-3 carry the thread's intra coordinate
-  int orem = o;
-  int ncoord[4] = {0, 0, 0, 0};
-#pragma unroll
-  for (int a = D - 3; a >= 0; --a) {
-    ncoord[a] = orem % E;
-    orem /= E;
-  }
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    int64_t c0 = gc[a] * E;
-    if (a < D - 2) {
-      int64_t c = c0 + ncoord[a];
-      if (c >= f.shape[a]) plane_valid = false;
-      off += c * f.stride[a];
-    } else {
-      off += c0 * f.stride[a];
-      if (c0 + E > f.shape[a]) interior = false;
+    if (a != P && a != Q) {
+      pos += (o % E) * axis_stride<D, E>(a);
+      o /= E;
     }
   }
+  return pos;
+}
+
+// fixed-axis coordinates of slice (P,Q) for thread o
+template <int D, int E, int P, int Q>
+__device__ __forceinline__ void slice_coords(int o, int (&c)[4]) {
+#pragma unroll
+  for (int a = D - 1; a >= 0; --a) {
+    if (a != P && a != Q) {
+      c[a] = o % E;
+      o /= E;
+    } else {
+      c[a] = 0;
+    }
+  }
+}
+
+// write slice (P,Q) of thread o into the block's canonical smem region
+template <int D, int E, int P, int Q>
+__device__ __forceinline__ void slice_store(double* blk, int swz, int o, const double* v) {
+  const int base = slice_base<D, E, P, Q>(o);
+#pragma unroll
+  for (int i = 0; i < E; ++i)
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+      blk[(base + i * axis_stride<D, E>(P) + j * axis_stride<D, E>(Q)) ^ swz] = v[i * E + j];
+}
+
+template <int D, int E, int P, int Q>
+__device__ __forceinline__ void slice_load(const double* blk, int swz, int o, double* v) {
+  const int base = slice_base<D, E, P, Q>(o);
+#pragma unroll
+  for (int i = 0; i < E; ++i)
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+      v[i * E + j] = blk[(base + i * axis_stride<D, E>(P) + j * axis_stride<D, E>(Q)) ^ swz];
+}
+
+// ------------------------------------------------- reference-exact lines --
+// forward: C[k] = fma chain over n of x[n] * H[n][k];  inverse: y[n] = fma
+// chain over k of C[k] * H[n][k]  (transforms.py:118-142 via dgemm order)
+template <int E, int S, bool INV>
+__device__ __forceinline__ void dense_line(double* v, const double (&H)[64]) {
+  double in[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) in[i] = v[i * S];
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    double acc = 0.0;
+#pragma unroll
+    for (int n = 0; n < E; ++n) acc = __fma_rn(in[n], INV ? H[k * E + n] : H[n * E + k], acc);
+    v[k * S] = acc;
+  }
+}
+
+// slice columns (lines over i, the P axis) / rows (lines over j, the Q axis)
+template <int E, bool INV>
+__device__ __forceinline__ void slice_cols(double* v, const double (&H)[64]) {
+#pragma unroll
+  for (int j = 0; j < E; ++j) dense_line<E, E, INV>(v + j, H);
+}
+template <int E, bool INV>
+__device__ __forceinline__ void slice_rows(double* v, const double (&H)[64]) {
+#pragma unroll
+  for (int i = 0; i < E; ++i) dense_line<E, 1, INV>(v + i * E, H);
+}
+
+// ------------------------------------------------ dense-side geometry ----
+// block coordinates of block b
+template <int D>
+__device__ __forceinline__ void block_coords(const FastGeo& f, int64_t b, int64_t (&gc)[4]) {
+#pragma unroll
+  for (int a = D - 1; a >= 0; --a) {
+    gc[a] = b % f.grid[a];
+    b /= f.grid[a];
+  }
+}
+
+// dense offset of slice (P, Q=D-1) element (0,0) at fixed coords c; whether
+// the whole slice is inside the array; per-row / per-column validity limits
+template <int D, int E, int P>
+__device__ __forceinline__ int64_t dense_slice_origin(const FastGeo& f, const int64_t (&gc)[4],
+                                                      const int (&c)[4], bool& interior,
+                                                      bool& fixed_ok, int& rows_ok,
+                                                      int& cols_ok) {
+  int64_t off = 0;
+  interior = true;
+  fixed_ok = true;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const int64_t c0 = gc[a] * E + c[a];
+    off += c0 * f.stride[a];
+    const int64_t room = f.shape[a] - gc[a] * E;  // valid coords along a within the block
+    if (a == P || a == D - 1) {
+      const int lim = room >= E ? E : (int)room;
+      if (a == P && a != D - 1) rows_ok = lim;
+      if (a == D - 1) cols_ok = lim;
+      if (lim < E) interior = false;
+    } else {
+      if (c[a] >= room) fixed_ok = false;
+    }
+  }
+  if (D == 1) rows_ok = 1;
+  return off;
 }
 
 // ------------------------------------------------ vector row load / store --
@@ -110,7 +210,7 @@ __device__ __forceinline__ void load_row_vec(const T* __restrict__ src, double* 
   static_assert(E % CH == 0, "row must be a whole number of 16-byte chunks");
 #pragma unroll
   for (int c = 0; c < E / CH; ++c) {
-    uint4 w = __ldg(reinterpret_cast<const uint4*>(src) + c);
+    uint4 w = __ldcs(reinterpret_cast<const uint4*>(src) + c);
     if constexpr (sizeof(T) == 4) {
       dst[c * 4 + 0] = (double)__uint_as_float(w.x);
       dst[c * 4 + 1] = (double)__uint_as_float(w.y);
@@ -146,11 +246,36 @@ __device__ __forceinline__ void store_row_vec(T* __restrict__ dst, const double*
 }
 
 template <typename T>
-constexpr bool row_vectorizable(int E) { return (E * (int)sizeof(T)) % 16 == 0; }
+__host__ __device__ constexpr bool row_vectorizable(int E) { return (E * (int)sizeof(T)) % 16 == 0; }
 
 // |x| as an ordered unsigned key: NaN > inf > finite
 __device__ __forceinline__ unsigned long long abs_key(double x) {
   return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+}
+
+// copy `nbytes` of a contiguous global range to / from shared memory; the
+// shared buffer is offset by `mis` = (global address mod 16) so that the
+// body moves as aligned 16-byte vectors
+__device__ __forceinline__ void tile_to_smem(unsigned char* st, const unsigned char* g,
+                                             int64_t nbytes, int mis, int t, int nt) {
+  const int head = mis ? 16 - mis : 0;
+  const int h = (int)min((int64_t)head, nbytes);
+  for (int i = t; i < h; i += nt) st[mis + i] = g[i];
+  const int64_t body = (nbytes - h) / 16;
+  for (int64_t i = t; i < body; i += nt)
+    *reinterpret_cast<uint4*>(st + mis + h + i * 16) = __ldcs(reinterpret_cast<const uint4*>(g + h) + i);
+  for (int64_t i = h + body * 16 + t; i < nbytes; i += nt) st[mis + i] = g[i];
+}
+
+__device__ __forceinline__ void smem_to_tile(unsigned char* g, const unsigned char* st,
+                                             int64_t nbytes, int mis, int t, int nt) {
+  const int head = mis ? 16 - mis : 0;
+  const int h = (int)min((int64_t)head, nbytes);
+  for (int i = t; i < h; i += nt) g[i] = st[mis + i];
+  const int64_t body = (nbytes - h) / 16;
+  for (int64_t i = t; i < body; i += nt)
+    __stcs(reinterpret_cast<uint4*>(g + h) + i, *reinterpret_cast<const uint4*>(st + mis + h + i * 16));
+  for (int64_t i = h + body * 16 + t; i < nbytes; i += nt) g[i] = st[mis + i];
 }
 
 }  // namespace bz

@@ -1,12 +1,13 @@
 // bz_fast_decompress.cu -- fused decompress: indices -> inverse transform ->
 // *N / r -> merge + crop, one pass (codec.py:364-384, arrays.py:181-190).
 //
-// Arithmetic follows the reference order: the inverse transform runs on the
-// raw integer indices and the block scale is applied after it as
-// fl(fl(y * N) / r) (codec.py:377-379).  The division by the constant r uses
-// Markstein's FMA correction (bz_common.cuh: div_const), which returns the
-// correctly rounded quotient; blocks whose N could push y*N out of the normal
-// range fall back to IEEE division.
+// Arithmetic is the reference's, step for step: the inverse transform runs on
+// the raw integer indices as the same FMA chain dgemm uses (axis 0 first,
+// bz_fast.cuh), then the block scale is applied as fl(fl(y * N) / r)
+// (codec.py:377-379).  The division by the constant r uses Markstein's FMA
+// correction (bz_common.cuh: div_const), which returns the correctly rounded
+// quotient; blocks whose N could push y*N out of the normal range use IEEE
+// division.  The f64 output is therefore bit-identical to the reference.
 #include "bz_fast.cuh"
 #include "bz_kernels.cuh"
 
@@ -17,7 +18,7 @@ __device__ __forceinline__ void load_indices_vec(const IT* __restrict__ src, dou
   static_assert((N * sizeof(IT)) % 16 == 0, "whole 16-byte chunks");
 #pragma unroll
   for (int c = 0; c < N * (int)sizeof(IT) / 16; ++c) {
-    uint4 w = __ldg(reinterpret_cast<const uint4*>(src) + c);
+    uint4 w = __ldcs(reinterpret_cast<const uint4*>(src) + c);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
     constexpr int PER = 16 / sizeof(IT);
 #pragma unroll
@@ -33,15 +34,18 @@ __device__ __forceinline__ void load_indices_vec(const IT* __restrict__ src, dou
   }
 }
 
-template <int D, int E, int FAM, typename IT, int FK, typename TOut>
+template <int D, int E, typename IT, int FK, typename TOut>
 __global__ void __launch_bounds__(Tile<D, E>::NT)
-k_fast_decompress(FastGeo f, const void* __restrict__ maxima, const IT* __restrict__ indices,
-                  TOut* __restrict__ out) {
+k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
+                  const IT* __restrict__ indices, TOut* __restrict__ out) {
   using TL = Tile<D, E>;
-  constexpr int NIN = TL::NIN, TB = TL::TB, M = TL::M, BPC = TL::BPC, NT = TL::NT;
+  constexpr int NIN = TL::NIN, BS = TL::BS, BPC = TL::BPC, NT = TL::NT;
+  constexpr int LP = 0, LQ = D - 1;                   // first slice (holds axis 0)
+  constexpr int SP = D >= 2 ? D - 2 : 0, SQ = D - 1;  // output slice
+  const FastGeo& f = p.f;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* xs = reinterpret_cast<double*>(smem_raw);
-  unsigned char* stage = smem_raw;
+  unsigned char* stage = smem_raw + (TL::EXCH ? (size_t)BPC * BS * sizeof(double) : 0);
 
   const int t = threadIdx.x;
   const int lb = t % BPC;
@@ -49,7 +53,8 @@ k_fast_decompress(FastGeo f, const void* __restrict__ maxima, const IT* __restri
   const double rr = radius_f64(sizeof(IT) == 1 ? BZ_I8 : (sizeof(IT) == 2 ? BZ_I16 : BZ_I32));
   const double rinv = 1.0 / rr;
   const double nsafe = 1.7976931348623157e308 / (rr * TL::BS * 4.0);
-  constexpr int SWZ = NIN >= 16 ? 15 : 0;
+  const int swz = lb & 15;
+  double* blk = xs + lb * BS;
   const bool stage_in = TL::EXCH || !f.full_mask;
 
   for (int64_t tile = blockIdx.x; tile < f.ntiles; tile += gridDim.x) {
@@ -58,149 +63,144 @@ k_fast_decompress(FastGeo f, const void* __restrict__ maxima, const IT* __restri
     const bool valid = b < f.nblocks;
     const int nvalid = (int)min((int64_t)BPC, f.nblocks - b0);
 
-    // ---- gather this thread's coefficients (as f64 integers)
-    double u[NIN];
+    // ---- first slice (axis 0, axis D-1) at o, as f64 integers
+    double v[NIN];
     if (stage_in) {
       const int64_t src_byte0 = b0 * (int64_t)f.kept * sizeof(IT);
       const int mis = (int)(((uintptr_t)indices + src_byte0) & 15);
-      const unsigned char* gsrc = reinterpret_cast<const unsigned char*>(indices) + src_byte0;
-      const int64_t nbytes = (int64_t)nvalid * f.kept * sizeof(IT);
-      const int head = mis ? 16 - mis : 0;
-      const int h = (int)min((int64_t)head, nbytes);
-      for (int i = t; i < h; i += NT) stage[mis + i] = gsrc[i];
-      const int64_t body = (nbytes - h) / 16;
-      for (int64_t i = t; i < body; i += NT)
-        *reinterpret_cast<uint4*>(stage + mis + h + i * 16) =
-            __ldg(reinterpret_cast<const uint4*>(gsrc + h) + i);
-      for (int64_t i = h + body * 16 + t; i < nbytes; i += NT) stage[mis + i] = gsrc[i];
+      tile_to_smem(stage, reinterpret_cast<const unsigned char*>(indices) + src_byte0,
+                   (int64_t)nvalid * f.kept * sizeof(IT), mis, t, NT);
       __syncthreads();
       const IT* st = reinterpret_cast<const IT*>(stage + mis);
+      const int base = D >= 2 ? slice_base<D, E, LP, LQ>(o) : 0;
 #pragma unroll
-      for (int o2 = 0; o2 < TB; ++o2)
+      for (int i = 0; i < (D >= 2 ? E : 1); ++i)
 #pragma unroll
-        for (int m = 0; m < M; ++m) {
-          const int pos = TL::EXCH ? o2 * NIN + o * M + m : m;
+        for (int j = 0; j < E; ++j) {
+          const int pos = base + i * axis_stride<D, E>(LP) * (D >= 2) + j * axis_stride<D, E>(LQ);
           const int rk = f.full_mask ? pos : f.rank[pos];
-          u[o2 * M + m] = (valid && rk >= 0) ? (double)st[lb * f.kept + rk] : 0.0;
+          v[i * E + j] = (valid && rk >= 0) ? (double)st[lb * f.kept + rk] : 0.0;
         }
-      __syncthreads();  // staging area becomes the exchange area
     } else {
       if (valid) {
         if constexpr ((NIN * sizeof(IT)) % 16 == 0) {
-          load_indices_vec<IT, NIN>(indices + b * (int64_t)NIN, u);
+          load_indices_vec<IT, NIN>(indices + b * (int64_t)NIN, v);
         } else {
 #pragma unroll
-          for (int p = 0; p < NIN; ++p) u[p] = (double)indices[b * (int64_t)NIN + p];
+          for (int q = 0; q < NIN; ++q) v[q] = (double)indices[b * (int64_t)NIN + q];
         }
       } else {
 #pragma unroll
-        for (int p = 0; p < NIN; ++p) u[p] = 0.0;
+        for (int q = 0; q < NIN; ++q) v[q] = 0.0;
       }
     }
 
-    // ---- inverse outer transform + exchange back to planes
-    double v[NIN];
-    if constexpr (TL::EXCH) {
-      if constexpr (D == 3) {
-#pragma unroll
-        for (int m = 0; m < M; ++m) iline<FAM, E, M>(u + m);
-      } else {
-        plane<FAM, E, true>(u);
-      }
-#pragma unroll
-      for (int o2 = 0; o2 < TB; ++o2)
-#pragma unroll
-        for (int m = 0; m < M; ++m)
-          xs[(lb * TB + o2) * NIN + ((o * M + m) ^ (lb & SWZ))] = u[o2 * M + m];
+    // ---- inverse transform, axis 0 first (reference order)
+    if constexpr (D == 1) {
+      dense_line<E, 1, true>(v, p.H);
+    } else if constexpr (D == 2) {
+      slice_cols<E, true>(v, p.H);
+      slice_rows<E, true>(v, p.H);
+    } else if constexpr (D == 3) {
+      slice_cols<E, true>(v, p.H);  // axis 0
+      slice_store<D, E, 0, 2>(blk, swz, o, v);
       __syncthreads();
-      const int row = lb * TB + o;
-#pragma unroll
-      for (int p = 0; p < NIN; ++p) v[p] = xs[row * NIN + (p ^ (lb & SWZ))];
+      slice_load<D, E, 1, 2>(blk, swz, o, v);
+      slice_cols<E, true>(v, p.H);  // axis 1
+      slice_rows<E, true>(v, p.H);  // axis 2
     } else {
-#pragma unroll
-      for (int p = 0; p < NIN; ++p) v[p] = u[p];
+      slice_cols<E, true>(v, p.H);  // axis 0
+      slice_store<D, E, 0, 3>(blk, swz, o, v);
+      __syncthreads();
+      slice_load<D, E, 1, 2>(blk, swz, o, v);
+      slice_cols<E, true>(v, p.H);  // axis 1
+      slice_rows<E, true>(v, p.H);  // axis 2
+      __syncthreads();
+      slice_store<D, E, 1, 2>(blk, swz, o, v);
+      __syncthreads();
+      slice_load<D, E, 2, 3>(blk, swz, o, v);
+      slice_rows<E, true>(v, p.H);  // axis 3
     }
-    if constexpr (D == 1) iline<FAM, E, 1>(v);
-    else plane<FAM, E, true>(v);
 
-    // ---- scale: ((y * N) / r), reference order
+    // ---- scale ((y * N) / r) and store the output slice (axis D-2 rows, D-1 cols)
     if (valid) {
       const double n = load_kind<FK>(maxima, b);
       const bool safe = (n >= 0x1p-900) && (n <= nsafe);
       if (safe) {
 #pragma unroll
-        for (int p = 0; p < NIN; ++p) v[p] = div_const(__dmul_rn(v[p], n), rr, rinv);
+        for (int q = 0; q < NIN; ++q) v[q] = div_const(__dmul_rn(v[q], n), rr, rinv);
       } else {
 #pragma unroll
-        for (int p = 0; p < NIN; ++p) v[p] = __ddiv_rn(__dmul_rn(v[p], n), rr);
+        for (int q = 0; q < NIN; ++q) v[q] = __ddiv_rn(__dmul_rn(v[q], n), rr);
       }
       if constexpr (sizeof(TOut) == 4) {
 #pragma unroll
-        for (int p = 0; p < NIN; ++p) v[p] = (double)__double2float_rn(v[p]);
+        for (int q = 0; q < NIN; ++q) v[q] = (double)__double2float_rn(v[q]);
       }
-
-      // ---- store the plane
-      int64_t off = 0, gc[4];
-      bool interior = false, pvalid = false;
-      plane_origin<D, E>(f, b, o, off, interior, pvalid, gc);
+      int64_t gc[4] = {0, 0, 0, 0};
+      int c[4];
+      slice_coords<D, E, SP, SQ>(o, c);
+      block_coords<D>(f, b, gc);
+      bool interior, fixed_ok;
+      int rows_ok = 0, cols_ok = 0;
+      const int64_t off = dense_slice_origin<D, E, SP>(f, gc, c, interior, fixed_ok, rows_ok, cols_ok);
       constexpr int ROWS = D >= 2 ? E : 1;
-      constexpr int RA = D >= 2 ? D - 2 : 0;
-      const int64_t rs = D >= 2 ? f.stride[RA] : 0;
-      if (pvalid) {
-        if (interior && row_vectorizable<TOut>(E) && f.vec_in) {
+      const int64_t rs = f.stride[SP];
+      if (fixed_ok) {
+        bool fast = false;
+        if constexpr (row_vectorizable<TOut>(E)) fast = interior && f.vec_dense;
+        if (fast) {
+          if constexpr (row_vectorizable<TOut>(E)) {
 #pragma unroll
-          for (int r = 0; r < ROWS; ++r) {
-            if constexpr (row_vectorizable<TOut>(E)) store_row_vec<TOut, E>(out + off + r * rs, v + r * E);
+            for (int r = 0; r < ROWS; ++r) store_row_vec<TOut, E>(out + off + r * rs, v + r * E);
           }
         } else {
 #pragma unroll
-          for (int r = 0; r < ROWS; ++r) {
+          for (int r = 0; r < ROWS; ++r)
 #pragma unroll
-            for (int cc = 0; cc < E; ++cc) {
-              bool in = true;
-              if (D >= 2) in = gc[RA] * E + r < f.shape[RA];
-              in = in && (gc[D - 1] * E + cc < f.shape[D - 1]);
-              if (in) out[off + r * rs + cc] = (TOut)v[r * E + cc];
-            }
-          }
+            for (int cc = 0; cc < E; ++cc)
+              if (r < rows_ok && cc < cols_ok) out[off + r * rs + cc] = (TOut)v[r * E + cc];
         }
       }
     }
-    if constexpr (TL::EXCH) __syncthreads();  // exchange area reused by the next tile
+    if (TL::EXCH || stage_in) __syncthreads();  // smem reused by the next tile
   }
 }
 
-template <int D, int E, int FAM, typename IT, int FK, typename TOut>
+template <int D, int E, typename IT, int FK, typename TOut>
 static int launch_one(const Geo& g, const void* maxima, const void* indices, void* out,
                       cudaStream_t s) {
   using TL = Tile<D, E>;
-  FastGeo f = make_fast_geo(g, TL::BPC, out, sizeof(TOut));
-  size_t smem = 0;
-  if (TL::EXCH) smem = (size_t)TL::NT * TL::NIN * sizeof(double);
-  if (TL::EXCH || !f.full_mask) smem = std::max(smem, (size_t)TL::BPC * g.kept * sizeof(IT) + 16);
-  auto kern = k_fast_decompress<D, E, FAM, IT, FK, TOut>;
+  FastParams p;
+  if (!make_fast_params(g, TL::BPC, out, sizeof(TOut), p)) {
+    set_error("fast decompress: host matrices missing");
+    return BZ_E_INVALID;
+  }
+  size_t smem = (TL::EXCH ? (size_t)TL::BPC * TL::BS * sizeof(double) : 0) +
+                ((TL::EXCH || !p.f.full_mask) ? (size_t)TL::BPC * g.kept * sizeof(IT) + 16 : 0);
+  auto kern = k_fast_decompress<D, E, IT, FK, TOut>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TL::NT, smem);
   if (occ < 1) occ = 1;
-  int64_t grid = std::min<int64_t>(f.ntiles, (int64_t)kSMs * occ);
+  int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * occ);
   if (grid < 1) return BZ_OK;
-  kern<<<(int)grid, TL::NT, smem, s>>>(f, maxima, reinterpret_cast<const IT*>(indices),
+  kern<<<(int)grid, TL::NT, smem, s>>>(p, maxima, reinterpret_cast<const IT*>(indices),
                                        reinterpret_cast<TOut*>(out));
   return check_launch("fast_decompress");
 }
 
-template <int D, int E, int FAM>
+template <int D, int E>
 static int dispatch_kinds(const Geo& g, const void* maxima, const void* indices, void* out,
                           int out_kind, cudaStream_t s) {
-#define BZ_OUT(IT, FKV)                                                                   \
-  if (out_kind == BZ_F64) return launch_one<D, E, FAM, IT, FKV, double>(g, maxima, indices, out, s); \
-  if (out_kind == BZ_F32) return launch_one<D, E, FAM, IT, FKV, float>(g, maxima, indices, out, s);
-#define BZ_IDX(FKV)                                    \
-  switch (g.index_kind) {                              \
-    case BZ_I8: { BZ_OUT(int8_t, FKV) break; }         \
-    case BZ_I16: { BZ_OUT(int16_t, FKV) break; }       \
-    case BZ_I32: { BZ_OUT(int32_t, FKV) break; }       \
+#define BZ_OUT(IT, FKV)                                                                        \
+  if (out_kind == BZ_F64) return launch_one<D, E, IT, FKV, double>(g, maxima, indices, out, s); \
+  if (out_kind == BZ_F32) return launch_one<D, E, IT, FKV, float>(g, maxima, indices, out, s);
+#define BZ_IDX(FKV)                              \
+  switch (g.index_kind) {                        \
+    case BZ_I8: { BZ_OUT(int8_t, FKV) break; }   \
+    case BZ_I16: { BZ_OUT(int16_t, FKV) break; } \
+    case BZ_I32: { BZ_OUT(int32_t, FKV) break; } \
   }
   if (g.float_kind == BZ_F32) { BZ_IDX(BZ_F32) }
   if (g.float_kind == BZ_F64) { BZ_IDX(BZ_F64) }
@@ -218,11 +218,8 @@ bool fast_decompress_supported(const Geo& g, int out_kind) {
 int launch_fast_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s) {
   const int E = g.block[0];
-  const bool haar = g.transform == BZ_HAAR;
-#define BZ_CASE(DD, EE)                                                                   \
-  if (g.ndim == DD && E == EE)                                                            \
-    return haar ? dispatch_kinds<DD, EE, HAAR>(g, maxima, indices, out, out_kind, s)      \
-                : dispatch_kinds<DD, EE, DCT>(g, maxima, indices, out, out_kind, s);
+#define BZ_CASE(DD, EE) \
+  if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, maxima, indices, out, out_kind, s);
   BZ_CASE(1, 4) BZ_CASE(1, 8) BZ_CASE(2, 4) BZ_CASE(2, 8) BZ_CASE(3, 4) BZ_CASE(3, 8)
   BZ_CASE(4, 4)
 #undef BZ_CASE

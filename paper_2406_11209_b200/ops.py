@@ -101,13 +101,21 @@ def _stream(a: CompressedArray) -> int:
     return _native.stream_handle(a.device)
 
 
+def _derive(a: CompressedArray, maxima, indices) -> CompressedArray:
+    """Result with a's shape/settings (and a's sharding, for sharded arrays)."""
+    hook = getattr(a, "_derive", None)
+    if hook is not None:
+        return hook(maxima, indices)
+    return CompressedArray(a.original_shape, a.settings, maxima, indices, _trusted=True)
+
+
 # ----------------------------------------------------------- elementwise ----
 def negate(a: CompressedArray) -> CompressedArray:
     """{s, N, -F}; exact (ops.py:195-197).  Maxima are shared."""
     out = torch.empty_like(a.indices)
     _native.call("bz_negate", a.settings.index_kind.code, a.indices.data_ptr(), out.data_ptr(),
                  a.indices.numel(), _stream(a))
-    return CompressedArray(a.original_shape, a.settings, a.maxima, out, _trusted=True)
+    return _derive(a, a.maxima, out)
 
 
 def _add(a: CompressedArray, b: CompressedArray, subtract: int) -> CompressedArray:
@@ -120,7 +128,7 @@ def _add(a: CompressedArray, b: CompressedArray, subtract: int) -> CompressedArr
     _native.call("bz_add", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
                  a.indices.data_ptr(), bm.data_ptr(), bi.data_ptr(), subtract,
                  out_max.data_ptr(), out_idx.data_ptr(), _stream(a))
-    return CompressedArray(a.original_shape, a.settings, out_max, out_idx, _trusted=True)
+    return _derive(a, out_max, out_idx)
 
 
 def add(a: CompressedArray, b: CompressedArray) -> CompressedArray:
@@ -142,7 +150,7 @@ def add_scalar(a: CompressedArray, x: float) -> CompressedArray:
     L = a.layout()
     _native.call("bz_add_scalar", ctypes.byref(L), a.maxima.data_ptr(), a.indices.data_ptr(),
                  shift, out_max.data_ptr(), out_idx.data_ptr(), _stream(a))
-    return CompressedArray(a.original_shape, a.settings, out_max, out_idx, _trusted=True)
+    return _derive(a, out_max, out_idx)
 
 
 def mul_scalar(a: CompressedArray, x: float) -> CompressedArray:
@@ -153,8 +161,7 @@ def mul_scalar(a: CompressedArray, x: float) -> CompressedArray:
     L = a.layout()
     _native.call("bz_mul_scalar", ctypes.byref(L), a.maxima.data_ptr(), a.indices.data_ptr(), x,
                  out_max.data_ptr(), None if out_idx is None else out_idx.data_ptr(), _stream(a))
-    return CompressedArray(a.original_shape, a.settings, out_max,
-                           a.indices if out_idx is None else out_idx, _trusted=True)
+    return _derive(a, out_max, a.indices if out_idx is None else out_idx)
 
 
 # ------------------------------------------------------------ reductions ----

@@ -40,8 +40,8 @@ def test_library_exports_every_declared_symbol():
 def test_layout_struct_matches_header():
     from paper_2406_11209_b200 import _native
 
-    # 4 int32 + 8 int64 + 8 int32 + 8 int64 + 2 int32 + 3 pointers
-    assert ctypes.sizeof(_native.Layout) == 16 + 64 + 32 + 64 + 8 + 24
+    # 4 int32 + 8 int64 + 8 int32 + 8 int64 + 2 int32 + 4 pointers
+    assert ctypes.sizeof(_native.Layout) == 16 + 64 + 32 + 64 + 8 + 32
     lib = _native.load_library(require_cuda=False)
     assert lib.bz_version() >= 10000
 

@@ -125,14 +125,10 @@ def test_fast_and_generic_agree(bz, monkeypatch, shape, block, fk, ik):
     generic = bz.compress(a, s)
     gen_dec = bz.decompress(fast).values
     monkeypatch.delenv("BZC_B200_FORCE_GENERIC")
-    if fk == "f64":
-        rel = ((fast.maxima - generic.maxima).abs() / generic.maxima.abs().clamp_min(1e-300)).max().item()
-        assert rel <= 1e-15
-    else:
-        assert torch.equal(fast.maxima, generic.maxima)
-    d = (fast.indices != generic.indices).double().mean().item()
-    assert d < 1e-5
-    assert ((fast_dec - gen_dec).abs().max() <= 1e-13 * gen_dec.abs().max()).item()
+    # both evaluate the reference's FMA chain: identical bits
+    assert torch.equal(fast.maxima, generic.maxima)
+    assert torch.equal(fast.indices, generic.indices)
+    assert torch.equal(fast_dec, gen_dec)
 
 
 # ------------------------------------------------------------- building blocks --
