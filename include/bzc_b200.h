@@ -79,6 +79,8 @@ typedef struct bz_layout {
 /* Library identification / diagnostics. */
 int bz_version(void);
 const char* bz_last_error(void);
+/* Number of kernels this library has launched in the process (benchmarks). */
+long long bz_launch_count(void);
 /* Which compress kernel a layout dispatches to: 1 = fused fast path, 0 = generic. */
 int bz_fast_path(const bz_layout* L);
 
@@ -126,7 +128,9 @@ int bz_add_scalar(const bz_layout* L, const void* maxima, const void* indices, d
  * When the mask drops the first coefficient, entries 1-5 are 0 and S_* run
  * over every kept position.  Records of shards merge with Chan's formulas.
  * `pair` = 0 reads only a (b ignored; *_b and *_ab mirror a).
- * dc_only = 1 computes entries 0-5 from the first coefficient only (mean).   */
+ * dc_only = 1 computes entries 0-5 from the first coefficient only (mean).
+ * The workspace must be zero-filled before its first use; the kernels leave
+ * it re-armed, so a caller keeps one workspace per stream.                  */
 size_t bz_moments_workspace(const bz_layout* L);
 int bz_moments(const bz_layout* La, const bz_layout* Lb, const void* a_max, const void* a_idx,
                const void* b_max, const void* b_idx, int pair, int dc_only, double* record,

@@ -61,6 +61,7 @@ _D = ctypes.c_double
 SIGNATURES = {
     "bz_version": (_I, []),
     "bz_last_error": (ctypes.c_char_p, []),
+    "bz_launch_count": (ctypes.c_longlong, []),
     "bz_fast_path": (_I, [_L]),
     "bz_compress_workspace": (_SZ, [_L]),
     "bz_compress": (_I, [_L, _P, _I, _P, _P, _P, _SZ, _P]),

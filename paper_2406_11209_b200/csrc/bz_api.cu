@@ -1,4 +1,5 @@
 // bz_api.cu -- extern "C" entry points (include/bzc_b200.h).
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -10,6 +11,7 @@
 namespace bz {
 
 static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -24,6 +26,7 @@ int check_launch(const char* what) {
     set_error("%s: %s", what, cudaGetErrorString(e));
     return BZ_E_CUDA;
   }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return BZ_OK;
 }
 
@@ -63,6 +66,7 @@ using namespace bz;
 extern "C" {
 
 int bz_version(void) { return 10000; }
+long long bz_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 const char* bz_last_error(void) { return g_err; }
 
 int bz_fast_path(const bz_layout* L) {
@@ -71,16 +75,15 @@ int bz_fast_path(const bz_layout* L) {
   return fast_supported(g, L->float_kind) ? 1 : 0;
 }
 
-// workspace for compress: special-block counter + list (fast path), or the
-// generic kernel's global scratch, or a pre-rounded copy of the input when its
-// kind differs from the float kind.
+// workspace for compress: the generic kernel's global scratch (very large
+// blocks only) or a pre-rounded copy of the input when its kind differs from
+// the float kind and the fused kernel handles the layout.
 size_t bz_compress_workspace(const bz_layout* L) {
   if (validate(L)) return 0;
   Geo g = make_geo(L);
-  size_t list = 16 + (size_t)g.nblocks * sizeof(int32_t);
   size_t generic = exact_compress_workspace(g, g.nblocks);
   size_t convert = (size_t)dense_count(L) * float_kind_bytes(L->float_kind) + 256;
-  return list + std::max(generic, convert) + 256;
+  return std::max(generic, convert) + 256;
 }
 
 int bz_compress(const bz_layout* L, const void* x, int x_kind, void* maxima, void* indices,
@@ -90,34 +93,17 @@ int bz_compress(const bz_layout* L, const void* x, int x_kind, void* maxima, voi
   Geo g = make_geo(L);
   if (g.nblocks == 0) return BZ_OK;
   cudaStream_t s = S(stream);
-  size_t list_bytes = 16 + (size_t)g.nblocks * sizeof(int32_t);
-  if (!ws || ws_bytes < list_bytes) { set_error("compress: workspace too small"); return BZ_E_WORKSPACE; }
-  int32_t* cnt = reinterpret_cast<int32_t*>(ws);
-  int32_t* list = cnt + 4;
-  unsigned char* rest = reinterpret_cast<unsigned char*>(ws) + ((list_bytes + 255) / 256) * 256;
-  size_t rest_bytes = ws_bytes - (rest - reinterpret_cast<unsigned char*>(ws));
-  const void* src = x;
-  int src_kind = x_kind;
   // input of another kind: convert_precision first (arrays.py:147-153)
-  if (x_kind != L->float_kind && !force_generic() &&
-      fast_supported(g, L->float_kind) && (L->float_kind == BZ_F32 || L->float_kind == BZ_F64)) {
+  if (x_kind != L->float_kind && !force_generic() && fast_supported(g, L->float_kind)) {
     size_t need = (size_t)dense_count(L) * float_kind_bytes(L->float_kind);
-    if (rest_bytes < need) { set_error("compress: workspace too small for conversion"); return BZ_E_WORKSPACE; }
-    if (int rc = launch_round_to_kind(x, x_kind, rest, L->float_kind, dense_count(L), nullptr, s)) return rc;
-    src = rest;
-    src_kind = L->float_kind;
-    rest += ((need + 255) / 256) * 256;
-    rest_bytes = ws_bytes - (rest - reinterpret_cast<unsigned char*>(ws));
+    if (!ws || ws_bytes < need) { set_error("compress: workspace too small for conversion"); return BZ_E_WORKSPACE; }
+    if (int rc = launch_round_to_kind(x, x_kind, ws, L->float_kind, dense_count(L), nullptr, s)) return rc;
+    return launch_fast_compress(g, ws, maxima, indices, s);
   }
-  if (!force_generic() && fast_supported(g, src_kind)) {
-    if (cudaMemsetAsync(cnt, 0, sizeof(int32_t), s) != cudaSuccess) return check_launch("memset");
-    if (int rc = launch_fast_compress(g, src, maxima, indices, cnt, list, s)) return rc;
-    // exact recomputation of flagged blocks (usually none)
-    return launch_exact_compress(g, src, src_kind, maxima, indices, list, cnt, g.nblocks / 64 + 1,
-                                 rest, rest_bytes, s);
-  }
-  return launch_exact_compress(g, x, x_kind, maxima, indices, nullptr, nullptr, g.nblocks, rest,
-                               rest_bytes, s);
+  if (!force_generic() && fast_supported(g, x_kind))
+    return launch_fast_compress(g, x, maxima, indices, s);
+  return launch_exact_compress(g, x, x_kind, maxima, indices, nullptr, nullptr, g.nblocks, ws,
+                               ws_bytes, s);
 }
 
 size_t bz_decompress_workspace(const bz_layout* L) {

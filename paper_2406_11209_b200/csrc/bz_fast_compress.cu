@@ -12,14 +12,15 @@
 // within W units of one half redo the reference's exact rint(fl(C / N) * r)
 // (codec.py:272-277), so every index equals the reference's.  Blocks whose
 // maximum is not finite, whose stored maximum is 0 / tiny, or whose stored
-// maximum rounds far below the true maximum are appended to a list and
-// recomputed by the exact generic kernel (bz_generic.cu).
+// maximum rounds far below the true maximum bin every coefficient with the
+// exact reference arithmetic (their coefficients already are the reference's).
 #include "bz_fast.cuh"
 #include "bz_kernels.cuh"
 
 namespace bz {
 
 // exact reference binning, out of line: reached for ~1e-5 of coefficients
+// and for every coefficient of a "special" block
 __device__ __noinline__ int bin_exact_call(double c, double n, double r) {
   return (int)bin_exact(c, n, r, r);
 }
@@ -40,7 +41,7 @@ __device__ __forceinline__ uint32_t idx_bits(int q) {
 template <int D, int E, typename TIn, int FK, typename IT>
 __global__ void __launch_bounds__(Tile<D, E>::NT)
 k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict__ maxima,
-                IT* __restrict__ indices, int32_t* special_count, int32_t* special_list) {
+                IT* __restrict__ indices) {
   using TL = Tile<D, E>;
   constexpr int NIN = TL::NIN, TB = TL::TB, BS = TL::BS, BPC = TL::BPC, NT = TL::NT;
   constexpr int LP = 0, LQ = D - 1;  // loaded slice axes
@@ -146,10 +147,7 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
                          (mx > n * 1.00390625);
     const double R = special ? 0.0 : __ddiv_rn(rr, n);
 
-    if (valid && o == 0) {
-      store_kind<FK>(maxima, b, n);
-      if (special) special_list[atomicAdd(special_count, 1)] = (int32_t)b;
-    }
+    if (valid && o == 0) store_kind<FK>(maxima, b, n);
 
     // ---- bin + store kept indices
     if (f.full_mask) {
@@ -162,14 +160,14 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
             uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int e = 0; e < PER; ++e) {
-              const int qv = special ? 0 : bin_one<IT>(v[cch * PER + e], R, n, rr);
+              const int qv = special ? bin_exact_call(v[cch * PER + e], n, rr) : bin_one<IT>(v[cch * PER + e], R, n, rr);
               w[(e * sizeof(IT)) / 4] |= idx_bits<IT>(qv) << ((e * sizeof(IT) * 8) % 32);
             }
             __stcs(reinterpret_cast<uint4*>(dst) + cch, make_uint4(w[0], w[1], w[2], w[3]));
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < NIN; ++q) dst[q] = (IT)(special ? 0 : bin_one<IT>(v[q], R, n, rr));
+          for (int q = 0; q < NIN; ++q) dst[q] = (IT)(special ? bin_exact_call(v[q], n, rr) : bin_one<IT>(v[q], R, n, rr));
         }
       }
     } else {
@@ -181,7 +179,7 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
 #pragma unroll
         for (int q = 0; q < NIN; ++q) {
           const int rk = f.rank[o * NIN + q];
-          if (rk >= 0) st[lb * f.kept + rk] = (IT)(special ? 0 : bin_one<IT>(v[q], R, n, rr));
+          if (rk >= 0) st[lb * f.kept + rk] = (IT)(special ? bin_exact_call(v[q], n, rr) : bin_one<IT>(v[q], R, n, rr));
         }
       }
       __syncthreads();
@@ -198,8 +196,7 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
 
 // ----------------------------------------------------------------- dispatch --
 template <int D, int E, typename TIn, int FK, typename IT>
-static int launch_one(const Geo& g, const void* x, void* maxima, void* indices, int32_t* cnt,
-                      int32_t* list, cudaStream_t s) {
+static int launch_one(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s) {
   using TL = Tile<D, E>;
   FastParams p;
   if (!make_fast_params(g, TL::BPC, x, sizeof(TIn), p)) {
@@ -217,18 +214,17 @@ static int launch_one(const Geo& g, const void* x, void* maxima, void* indices, 
   int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * occ);
   if (grid < 1) return BZ_OK;
   kern<<<(int)grid, TL::NT, smem, s>>>(p, reinterpret_cast<const TIn*>(x), maxima,
-                                       reinterpret_cast<IT*>(indices), cnt, list);
+                                       reinterpret_cast<IT*>(indices));
   return check_launch("fast_compress");
 }
 
 template <int D, int E>
-static int dispatch_kinds(const Geo& g, const void* x, void* maxima, void* indices, int32_t* cnt,
-                          int32_t* list, cudaStream_t s) {
+static int dispatch_kinds(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s) {
 #define BZ_IDX(TIN, FKV)                                                                      \
   switch (g.index_kind) {                                                                     \
-    case BZ_I8: return launch_one<D, E, TIN, FKV, int8_t>(g, x, maxima, indices, cnt, list, s);   \
-    case BZ_I16: return launch_one<D, E, TIN, FKV, int16_t>(g, x, maxima, indices, cnt, list, s); \
-    case BZ_I32: return launch_one<D, E, TIN, FKV, int32_t>(g, x, maxima, indices, cnt, list, s); \
+    case BZ_I8: return launch_one<D, E, TIN, FKV, int8_t>(g, x, maxima, indices, s);   \
+    case BZ_I16: return launch_one<D, E, TIN, FKV, int16_t>(g, x, maxima, indices, s); \
+    case BZ_I32: return launch_one<D, E, TIN, FKV, int32_t>(g, x, maxima, indices, s); \
   }
   if (g.float_kind == BZ_F32) { BZ_IDX(float, BZ_F32) }
   if (g.float_kind == BZ_F64) { BZ_IDX(double, BZ_F64) }
@@ -260,12 +256,11 @@ bool fast_supported(const Geo& g, int x_kind) {
   return false;
 }
 
-int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices,
-                         int32_t* cnt, int32_t* list, cudaStream_t s) {
+int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s) {
   int E;
   uniform_block(g, E);
 #define BZ_CASE(DD, EE) \
-  if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, x, maxima, indices, cnt, list, s);
+  if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, x, maxima, indices, s);
   BZ_CASE(1, 4) BZ_CASE(1, 8) BZ_CASE(2, 4) BZ_CASE(2, 8) BZ_CASE(3, 4) BZ_CASE(3, 8)
   BZ_CASE(4, 4)
 #undef BZ_CASE

@@ -32,8 +32,7 @@ int launch_exact_decompress(const Geo& g, const void* maxima, const void* indice
 
 // fused fast paths (bz_fast_*.cu)
 bool fast_supported(const Geo& g, int x_kind);
-int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices,
-                         int32_t* special_count, int32_t* special_list, cudaStream_t s);
+int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s);
 bool fast_decompress_supported(const Geo& g, int out_kind);
 int launch_fast_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s);

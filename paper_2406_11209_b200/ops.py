@@ -215,6 +215,20 @@ def merge_records(records) -> Record:
     return acc if acc is not None else Record(0, 0, 0, 0, 0, 0, 0, 0, 0)
 
 
+_REDUCE_WS: dict = {}
+
+
+def _reduce_workspace(dev: torch.device, nbytes: int) -> torch.Tensor:
+    """Zero-initialised, persistent per (device, stream) workspace: the
+    reduction kernels leave their ticket counter re-armed (include/bzc_b200.h)."""
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    ws = _REDUCE_WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        _REDUCE_WS[key] = ws
+    return ws
+
+
 def moments_record(a: CompressedArray, b: CompressedArray | None = None, *,
                    dc_only: bool = False) -> torch.Tensor:
     """Launch the fused reduction; returns the device record (16 float64)."""
@@ -239,7 +253,7 @@ def moments_record(a: CompressedArray, b: CompressedArray | None = None, *,
             from .codec import layout as _layout
 
             Lb = _layout(b.settings, b.original_shape, dev, index_kind=wide)
-    ws = workspace(_native.query("bz_moments_workspace", ctypes.byref(La)), dev)
+    ws = _reduce_workspace(dev, _native.query("bz_moments_workspace", ctypes.byref(La)))
     _native.call("bz_moments", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
                  a.indices.data_ptr(), bm.data_ptr() if pair else None,
                  bi.data_ptr() if pair else None, int(pair), int(dc_only), rec.data_ptr(),
