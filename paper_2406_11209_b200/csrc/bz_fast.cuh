@@ -248,6 +248,32 @@ __device__ __forceinline__ void store_row_vec(T* __restrict__ dst, const double*
 template <typename T>
 __host__ __device__ constexpr bool row_vectorizable(int E) { return (E * (int)sizeof(T)) % 16 == 0; }
 
+// ------------------------------------------------------------- cp.async --
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <typename T>
+__device__ __forceinline__ void unpack_row(const uint4* src, double* dst, int units) {
+  // units 16-byte chunks of T -> doubles
+#pragma unroll
+  for (int c = 0; c < units; ++c) {
+    const uint4 w = src[c];
+    if constexpr (sizeof(T) == 4) {
+      dst[c * 4 + 0] = (double)__uint_as_float(w.x);
+      dst[c * 4 + 1] = (double)__uint_as_float(w.y);
+      dst[c * 4 + 2] = (double)__uint_as_float(w.z);
+      dst[c * 4 + 3] = (double)__uint_as_float(w.w);
+    } else {
+      dst[c * 2 + 0] = __hiloint2double((int)w.y, (int)w.x);
+      dst[c * 2 + 1] = __hiloint2double((int)w.w, (int)w.z);
+    }
+  }
+}
+
 // |x| as an ordered unsigned key: NaN > inf > finite
 __device__ __forceinline__ unsigned long long abs_key(double x) {
   return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;

@@ -59,43 +59,76 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
   const int swz = lb & 15;
   double* blk = xs + lb * BS;
 
+  // per-thread private prefetch stage: the next tile's slice rows arrive by
+  // cp.async while the current tile computes (interleaved by thread, so the
+  // 16-byte reads are bank-conflict free)
+  constexpr int ROWS = D >= 2 ? E : 1;
+  constexpr bool VEC = row_vectorizable<TIn>(E);
+  constexpr int RU = VEC ? E * (int)sizeof(TIn) / 16 : 1;  // 16-byte units per row
+  uint4* pstage = reinterpret_cast<uint4*>(stage + (f.full_mask ? 0 : ((size_t)BPC * f.kept * sizeof(IT) + 16 + 15) / 16 * 16));
+  int c[4];
+  slice_coords<D, E, LP, LQ>(o, c);
+  const int64_t rs = f.stride[0];
+
+  // geometry of this thread's slice in `tile`; true when the slice is a run
+  // of whole, aligned, in-bounds 16-byte rows
+  auto geom = [&](int64_t tile, int64_t& off, bool& fixed_ok, int& rows_ok, int& cols_ok) {
+    const int64_t b = tile * BPC + lb;
+    off = 0;
+    fixed_ok = false;
+    rows_ok = cols_ok = 0;
+    if (tile >= f.ntiles || b >= f.nblocks) return false;
+    int64_t gc[4] = {0, 0, 0, 0};
+    block_coords<D>(f, b, gc);
+    bool interior;
+    off = dense_slice_origin<D, E, LP>(f, gc, c, interior, fixed_ok, rows_ok, cols_ok);
+    return VEC && fixed_ok && interior && f.vec_dense;
+  };
+  auto prefetch = [&](int64_t tile) {
+    int64_t off;
+    bool fok;
+    int ro, co;
+    const bool fast = geom(tile, off, fok, ro, co);
+    if (fast) {
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+        for (int u = 0; u < RU; ++u)
+          cp_async16(pstage + (r * RU + u) * NT + t, x + off + r * rs + u * (16 / sizeof(TIn)));
+    }
+    cp_async_commit();
+    return fast;
+  };
+
+  bool pf = prefetch(blockIdx.x);
   for (int64_t tile = blockIdx.x; tile < f.ntiles; tile += gridDim.x) {
     const int64_t b0 = tile * BPC;
     const int64_t b = b0 + lb;
     const bool valid = b < f.nblocks;
     const int nvalid = (int)min((int64_t)BPC, f.nblocks - b0);
 
-    // ---- load slice (axis 0, axis D-1) at fixed coords o
+    // ---- slice (axis 0, axis D-1) at fixed coords o: from the stage, or
+    //      direct guarded loads for partial / unaligned blocks
     double v[NIN];
-    {
-      int64_t gc[4] = {0, 0, 0, 0};
-      int c[4];
-      slice_coords<D, E, LP, LQ>(o, c);
-      bool interior = false, fixed_ok = false;
-      int rows_ok = 0, cols_ok = 0;
-      int64_t off = 0;
-      if (valid) {
-        block_coords<D>(f, b, gc);
-        off = dense_slice_origin<D, E, LP>(f, gc, c, interior, fixed_ok, rows_ok, cols_ok);
-      }
-      constexpr int ROWS = D >= 2 ? E : 1;
-      const int64_t rs = f.stride[0];
-      bool fast = false;
-      if constexpr (row_vectorizable<TIn>(E)) fast = valid && fixed_ok && interior && f.vec_dense;
-      if (fast) {
-        if constexpr (row_vectorizable<TIn>(E)) {
+    if (pf) {
+      cp_async_wait_all();
+      uint4 w[ROWS * RU];
 #pragma unroll
-          for (int r = 0; r < ROWS; ++r) load_row_vec<TIn, E>(x + off + r * rs, v + r * E);
-        }
-      } else {
+      for (int k = 0; k < ROWS * RU; ++k) w[k] = pstage[k * NT + t];
 #pragma unroll
-        for (int r = 0; r < ROWS; ++r)
+      for (int r = 0; r < ROWS; ++r) unpack_row<TIn>(w + r * RU, v + r * E, RU);
+    } else {
+      int64_t off;
+      bool fok;
+      int ro, co;
+      geom(tile, off, fok, ro, co);
 #pragma unroll
-          for (int cc = 0; cc < E; ++cc)
-            v[r * E + cc] = (valid && fixed_ok && r < rows_ok && cc < cols_ok)
-                                ? widen(x[off + r * rs + cc]) : 0.0;
-      }
+      for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+        for (int cc = 0; cc < E; ++cc)
+          v[r * E + cc] = (valid && fok && r < ro && cc < co) ? widen(x[off + r * rs + cc]) : 0.0;
     }
+    pf = prefetch(tile + gridDim.x);  // stage reads above have completed (values in use)
 
     // ---- forward transform, axis 0 first (reference order)
     if constexpr (D == 1) {
@@ -203,9 +236,12 @@ static int launch_one(const Geo& g, const void* x, void* maxima, void* indices, 
     set_error("fast compress: host matrices missing");
     return BZ_E_INVALID;
   }
+  constexpr int ROWS = D >= 2 ? E : 1;
+  constexpr int RU = row_vectorizable<TIn>(E) ? E * (int)sizeof(TIn) / 16 : 1;
   size_t smem = (TL::EXCH ? (size_t)TL::BPC * TL::BS * sizeof(double) : 0) +
                 (TL::TB > 1 ? (size_t)TL::NT * 8 : 0) +
-                (p.f.full_mask ? 0 : (size_t)TL::BPC * g.kept * sizeof(IT) + 16);
+                (p.f.full_mask ? 0 : ((size_t)TL::BPC * g.kept * sizeof(IT) + 16 + 15) / 16 * 16) +
+                (size_t)TL::NT * ROWS * RU * 16;
   auto kern = k_fast_compress<D, E, TIn, FK, IT>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;

@@ -45,7 +45,9 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
   const FastGeo& f = p.f;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* xs = reinterpret_cast<double*>(smem_raw);
-  unsigned char* stage = smem_raw + (TL::EXCH ? (size_t)BPC * BS * sizeof(double) : 0);
+  // two index-tile buffers: tile t+1 streams in (cp.async) while tile t computes
+  const size_t stage_bytes = ((size_t)BPC * f.kept * sizeof(IT) + 16 + 15) / 16 * 16;
+  unsigned char* stages = smem_raw + (TL::EXCH ? (size_t)BPC * BS * sizeof(double) : 0);
 
   const int t = threadIdx.x;
   const int lb = t % BPC;
@@ -57,21 +59,42 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
   double* blk = xs + lb * BS;
   const bool stage_in = TL::EXCH || !f.full_mask;
 
-  for (int64_t tile = blockIdx.x; tile < f.ntiles; tile += gridDim.x) {
+  // copy a tile's kept indices into stage buffer `buf` (body by cp.async)
+  auto prefetch = [&](int64_t tile, int buf) {
+    if (tile < f.ntiles) {
+      const int64_t b0 = tile * BPC;
+      const int nv = (int)min((int64_t)BPC, f.nblocks - b0);
+      const int64_t byte0 = b0 * (int64_t)f.kept * sizeof(IT);
+      const int64_t nbytes = (int64_t)nv * f.kept * sizeof(IT);
+      const int mis = (int)(((uintptr_t)indices + byte0) & 15);
+      const unsigned char* g = reinterpret_cast<const unsigned char*>(indices) + byte0;
+      unsigned char* st = stages + buf * stage_bytes;
+      const int head = mis ? 16 - mis : 0;
+      const int h = (int)min((int64_t)head, nbytes);
+      for (int i = t; i < h; i += NT) st[mis + i] = g[i];
+      const int64_t body = (nbytes - h) / 16;
+      for (int64_t i = t; i < body; i += NT) cp_async16(st + mis + h + i * 16, g + h + i * 16);
+      for (int64_t i = h + body * 16 + t; i < nbytes; i += NT) st[mis + i] = g[i];
+    }
+    cp_async_commit();
+  };
+
+  int buf = 0;
+  if (stage_in) prefetch(blockIdx.x, 0);
+  for (int64_t tile = blockIdx.x; tile < f.ntiles; tile += gridDim.x, buf ^= 1) {
     const int64_t b0 = tile * BPC;
     const int64_t b = b0 + lb;
     const bool valid = b < f.nblocks;
-    const int nvalid = (int)min((int64_t)BPC, f.nblocks - b0);
 
     // ---- first slice (axis 0, axis D-1) at o, as f64 integers
     double v[NIN];
     if (stage_in) {
+      cp_async_wait_all();
+      __syncthreads();
+      prefetch(tile + gridDim.x, buf ^ 1);
       const int64_t src_byte0 = b0 * (int64_t)f.kept * sizeof(IT);
       const int mis = (int)(((uintptr_t)indices + src_byte0) & 15);
-      tile_to_smem(stage, reinterpret_cast<const unsigned char*>(indices) + src_byte0,
-                   (int64_t)nvalid * f.kept * sizeof(IT), mis, t, NT);
-      __syncthreads();
-      const IT* st = reinterpret_cast<const IT*>(stage + mis);
+      const IT* st = reinterpret_cast<const IT*>(stages + buf * stage_bytes + mis);
       const int base = D >= 2 ? slice_base<D, E, LP, LQ>(o) : 0;
 #pragma unroll
       for (int i = 0; i < (D >= 2 ? E : 1); ++i)
@@ -163,7 +186,7 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
         }
       }
     }
-    if (TL::EXCH || stage_in) __syncthreads();  // smem reused by the next tile
+    if (TL::EXCH) __syncthreads();  // exchange area reused by the next tile
   }
 }
 
@@ -177,7 +200,8 @@ static int launch_one(const Geo& g, const void* maxima, const void* indices, voi
     return BZ_E_INVALID;
   }
   size_t smem = (TL::EXCH ? (size_t)TL::BPC * TL::BS * sizeof(double) : 0) +
-                ((TL::EXCH || !p.f.full_mask) ? (size_t)TL::BPC * g.kept * sizeof(IT) + 16 : 0);
+                ((TL::EXCH || !p.f.full_mask)
+                     ? 2 * (((size_t)TL::BPC * g.kept * sizeof(IT) + 16 + 15) / 16 * 16) : 0);
   auto kern = k_fast_decompress<D, E, IT, FK, TOut>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;

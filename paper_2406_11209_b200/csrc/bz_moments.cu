@@ -234,12 +234,14 @@ __device__ __forceinline__ long long first_elem(const uint4& w) {
   else return (long long)(((unsigned long long)w.y << 32) | w.x);
 }
 
-template <typename IT>
+template <typename IT, bool PAIR>
 __device__ __forceinline__ void part_reduce(Part<IT>& p, unsigned mask, int width) {
   for (int o = width / 2; o > 0; o >>= 1) {
-    p.ab += __shfl_xor_sync(mask, p.ab, o, width);
     p.aa += __shfl_xor_sync(mask, p.aa, o, width);
-    p.bb += __shfl_xor_sync(mask, p.bb, o, width);
+    if (PAIR) {
+      p.ab += __shfl_xor_sync(mask, p.ab, o, width);
+      p.bb += __shfl_xor_sync(mask, p.bb, o, width);
+    }
   }
 }
 
@@ -271,12 +273,17 @@ k_moments_vec(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
   const int lane = threadIdx.x & 31;
   const int sub = lane % GS;
   const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1) << (lane - sub));
-  const int64_t group = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GS;
-  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / GS;
+  constexpr int GPW = 32 / GS;  // groups per warp
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int gw = lane / GS;       // group within the warp
   const int nch = kept / (GS * V);  // chunks per lane per block
   const bool dc = keeps_first != 0;
   MomState st;
-  for (int64_t bb = group * U; bb < nblocks; bb += ngroups * U) {
+  // the warp owns U*GPW consecutive blocks per iteration; block of (u, group)
+  // is base + u*GPW + gw, so every load instruction covers a contiguous range
+  for (int64_t base = warp * (U * GPW); base < nblocks; base += nwarps * (U * GPW)) {
+    const int64_t bb = base + gw;  // block for u is bb + u*GPW
     double na[U], nb[U];
     Part<IT> p[U];
     using F0 = typename std::conditional<sizeof(IT) == 8, long long, int>::type;
@@ -285,17 +292,17 @@ k_moments_vec(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
     for (int u = 0; u < U; ++u) {
       na[u] = nb[u] = 0.0;
       f0a[u] = f0b[u] = 0;
-      if (sub == 0 && bb + u < nblocks) {
-        na[u] = load_kind_rt(a_max, bb + u, fk_a);
-        nb[u] = PAIR ? load_kind_rt(b_max, bb + u, fk_b) : na[u];
+      if (sub == 0 && bb + u * GPW < nblocks) {
+        na[u] = load_kind_rt(a_max, bb + u * GPW, fk_a);
+        nb[u] = PAIR ? load_kind_rt(b_max, bb + u * GPW, fk_b) : na[u];
       }
     }
     for (int ch = 0; ch < nch; ++ch) {
       uint4 wa[U], wb[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t off = (bb + u) * (int64_t)kept + (int64_t)(ch * GS + sub) * V;
-        const bool ok = bb + u < nblocks;
+        const int64_t off = (bb + u * GPW) * (int64_t)kept + (int64_t)(ch * GS + sub) * V;
+        const bool ok = bb + u * GPW < nblocks;
         wa[u] = ok ? __ldcs(reinterpret_cast<const uint4*>(a_idx + off)) : make_uint4(0, 0, 0, 0);
         wb[u] = (PAIR && ok) ? __ldcs(reinterpret_cast<const uint4*>(b_idx + off)) : wa[u];
       }
@@ -310,8 +317,8 @@ k_moments_vec(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      part_reduce<IT>(p[u], gmask, GS);
-      if (sub == 0 && bb + u < nblocks) {
+      part_reduce<IT, PAIR>(p[u], gmask, GS);
+      if (sub == 0 && bb + u * GPW < nblocks) {
         double iab, iaa, ibb;
         part_values<IT>(p[u], (double)f0a[u], (double)f0b[u], dc, iab, iaa, ibb);
         st.add_block(iab, iaa, ibb, (double)f0a[u], (double)f0b[u], na[u], nb[u], dc);
@@ -467,11 +474,13 @@ static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const v
                        !(((uintptr_t)a_idx | (PAIR ? (uintptr_t)b_idx : 0)) & 15);
   if (aligned) {
     const int vecs = kept / V;  // 16-byte chunks per block
-    int GS = 1;
-    while (GS < 32 && GS < vecs) GS <<= 1;
-    if (vecs % GS) GS = 1;  // chunks must split evenly over the group
+    int GS = 1;  // blocks of <= 64 bytes: one lane owns whole blocks
+    if (vecs > 4) {
+      while (GS < 32 && GS < vecs) GS <<= 1;
+      if (vecs % GS) GS = 1;  // chunks must split evenly over the group
+    }
     constexpr int U = PAIR ? 2 : 4;
-    const int64_t work = (B * GS + 256 * U - 1) / (256 * U);
+    const int64_t work = (B * GS + 256 * U - 1) / (256 * U);  // CTAs for one sweep
 #define BZ_GS(G)                                                                          \
   case G: {                                                                               \
     auto kern = k_moments_vec<IT, G, U, PAIR>;                                            \

@@ -122,48 +122,42 @@ __device__ __noinline__ long long bin_exact_out(double c, double n, double r, do
   return bin_exact(c, n, r, bound);
 }
 
-// coefficients of one chunk: ((F*N)/r) for a and b, summed -- reference order
-template <typename IT>
-__device__ __forceinline__ void chunk_coeffs(const elem_t<IT> (&fa)[16 / sizeof(IT)],
-                                             const elem_t<IT> (&fb)[16 / sizeof(IT)], double na,
-                                             double nb, double r, double rinv, bool safe,
-                                             int mode, int subtract, double shift, int k0,
-                                             double (&c)[16 / sizeof(IT)]) {
-  constexpr int V = 16 / sizeof(IT);
-  if (safe) {
-#pragma unroll
-    for (int e = 0; e < V; ++e) {
-      const double ca = div_const(__dmul_rn((double)fa[e], na), r, rinv);
-      if (mode == 0) {
-        const double fbv = subtract ? -(double)fb[e] : (double)fb[e];
-        c[e] = __dadd_rn(ca, div_const(__dmul_rn(fbv, nb), r, rinv));
-      } else {
-        c[e] = (k0 + e == 0) ? __dadd_rn(ca, shift) : ca;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < V; ++e) {
-      const double ca = spec_coeff_slow((double)fa[e], na, r);
-      if (mode == 0) {
-        const double fbv = subtract ? -(double)fb[e] : (double)fb[e];
-        c[e] = __dadd_rn(ca, spec_coeff_slow(fbv, nb, r));
-      } else {
-        c[e] = (k0 + e == 0) ? __dadd_rn(ca, shift) : ca;
-      }
-    }
-  }
+// F*N exactly as the reference's fl(float(F) * N): for |F| < 2^31 the
+// integer is widened with the 2^52+2^31 bias trick (an integer op + the FMA
+// below) instead of the slow int->f64 conversion; when N has <= 31
+// significant bits (every BF16/F16/F32 maximum), bias*N is exact and
+// fma(biased, N, -bias*N) = RN(F*N) in one DFMA.
+struct Scale {
+  double n, nbias;  // N and -(2^52+2^31)*N (exact when narrow)
+  bool narrow;      // N fits 31 significant bits
+};
+__device__ __forceinline__ Scale make_scale(double n, int fk) {
+  Scale s;
+  s.n = n;
+  s.narrow = fk != BZ_F64;
+  s.nbias = -(4503601774854144.0 * n);
+  return s;
+}
+__device__ __forceinline__ double fn_product(int f, const Scale& s) {
+  const double biased = __hiloint2double(0x43300000, (int)((unsigned)f ^ 0x80000000u));
+  if (s.narrow) return __fma_rn(biased, s.n, s.nbias);
+  return __dmul_rn(biased - 4503601774854144.0, s.n);
+}
+__device__ __forceinline__ double fn_product(long long f, const Scale& s) {
+  return __dmul_rn((double)f, s.n);
 }
 
 // mode 0: a + (+/-)b     mode 1: a + shift at the first coefficient (add_scalar)
-template <typename IT, int GS>
+// A group of GS lanes handles one block; each lane keeps NCH chunks of V
+// coefficients in registers (GS*NCH*V >= kept), so the block is read once.
+template <typename IT, int GS, int NCH>
 __global__ void __launch_bounds__(256)
 k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
       const void* __restrict__ a_max, const IT* __restrict__ a_idx,
       const void* __restrict__ b_max, const IT* __restrict__ b_idx, int subtract,
       double shift, int mode, void* __restrict__ out_max, IT* __restrict__ out_idx, bool vec) {
   constexpr int V = 16 / sizeof(IT);
-  constexpr int CH = GS * V;  // elements per chunk
+  constexpr int L = NCH * V;  // coefficients per lane
   constexpr int IK = sizeof(IT) == 1 ? BZ_I8 : sizeof(IT) == 2 ? BZ_I16 : sizeof(IT) == 4 ? BZ_I32 : BZ_I64;
   using FB_T = typename std::conditional<sizeof(IT) == 8, int32_t, IT>::type;
   const double r = radius_f64(IK), bound = clamp_bound_f64(IK);
@@ -173,32 +167,44 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
   const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1) << (lane - sub));
   const int64_t group = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GS;
   const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / GS;
-  const int nchunks = (kept + CH - 1) / CH;
-  const int64_t iters = (nblocks + ngroups - 1) / ngroups;
-  for (int64_t it = 0; it < iters; ++it) {
-    const int64_t b = group + it * ngroups;
-    const bool valid = b < nblocks;
-    const int64_t base = (valid ? b : 0) * (int64_t)kept;
-    const int kv = valid ? kept : 0;
-    double na = 0.0, nb = 0.0;
-    if (valid) {
-      na = load_kind_rt(a_max, b, fk_a);
-      if (mode == 0) nb = load_kind_rt(b_max, b, fk_b);
-    }
+  for (int64_t b = group; b < nblocks; b += ngroups) {
+    const int64_t base = b * (int64_t)kept;
+    const double na = load_kind_rt(a_max, b, fk_a);
+    const double nb = mode == 0 ? load_kind_rt(b_max, b, fk_b) : 0.0;
+    const Scale sa = make_scale(na, fk_a), sb = make_scale(nb, fk_b);
     const bool safe = na >= 0x1p-900 && na <= 0x1p+900 &&
                       (mode != 0 || (nb >= 0x1p-900 && nb <= 0x1p+900));
-    double c[V];
-    elem_t<IT> fa[V], fb[V];
+    double c[L];
     unsigned long long key = 0;
-    for (int ch = 0; ch < nchunks; ++ch) {
-      const int k0 = ch * CH + sub * V;
-      load_chunk<IT>(a_idx, base, k0, kv, vec, fa);
-      if (mode == 0) load_chunk<IT>(b_idx, base, k0, kv, vec, fb);
-      chunk_coeffs<IT>(fa, fb, na, nb, r, rinv, safe, mode, subtract, shift, k0, c);
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int k0 = (ch * GS + sub) * V;
+      elem_t<IT> fa[V], fb[V];
+      load_chunk<IT>(a_idx, base, k0, kept, vec, fa);
+      if (mode == 0) load_chunk<IT>(b_idx, base, k0, kept, vec, fb);
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        if (k0 + e < kv) {
-          const unsigned long long k2 = (unsigned long long)__double_as_longlong(c[e]) & 0x7fffffffffffffffull;
+        double cc;
+        if (safe) {
+          const double ca = div_const(fn_product(fa[e], sa), r, rinv);
+          if (mode == 0) {
+            const elem_t<IT> fbv = subtract ? -fb[e] : fb[e];
+            cc = __dadd_rn(ca, div_const(fn_product(fbv, sb), r, rinv));
+          } else {
+            cc = (k0 + e == 0) ? __dadd_rn(ca, shift) : ca;
+          }
+        } else {
+          const double ca = spec_coeff_slow((double)fa[e], na, r);
+          if (mode == 0) {
+            const double fbv = subtract ? -(double)fb[e] : (double)fb[e];
+            cc = __dadd_rn(ca, spec_coeff_slow(fbv, nb, r));
+          } else {
+            cc = (k0 + e == 0) ? __dadd_rn(ca, shift) : ca;
+          }
+        }
+        c[ch * V + e] = cc;
+        if (k0 + e < kept) {
+          const unsigned long long k2 = (unsigned long long)__double_as_longlong(cc) & 0x7fffffffffffffffull;
           key = k2 > key ? k2 : key;
         }
       }
@@ -210,53 +216,47 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
     }
     const double mx = __longlong_as_double((long long)key);  // NaN-propagating via bit order
     const double n = round_to_kind_rt(mx, fk_out);
-    if (valid && sub == 0) store_kind_rt(out_max, b, n, fk_out);
+    if (sub == 0) store_kind_rt(out_max, b, n, fk_out);
     const bool special = sizeof(IT) == 8 || !(mx <= 1.7976931348623157e308) ||
                          !(n >= 0x1p-1000) || (mx > n * 1.00390625);
     const double R = special ? 0.0 : __ddiv_rn(r, n);
-    for (int ch = 0; ch < nchunks; ++ch) {
-      const int k0 = ch * CH + sub * V;
-      if (nchunks > 1) {  // recompute this chunk's coefficients
-        load_chunk<IT>(a_idx, base, k0, kv, vec, fa);
-        if (mode == 0) load_chunk<IT>(b_idx, base, k0, kv, vec, fb);
-        chunk_coeffs<IT>(fa, fb, na, nb, r, rinv, safe, mode, subtract, shift, k0, c);
-      }
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int k0 = (ch * GS + sub) * V;
       long long q[V];
       if (special) {
 #pragma unroll
-        for (int e = 0; e < V; ++e) q[e] = bin_exact_out(c[e], n, r, bound);
+        for (int e = 0; e < V; ++e) q[e] = bin_exact_out(c[ch * V + e], n, r, bound);
       } else {
         bool near = false;
 #pragma unroll
-        for (int e = 0; e < V; ++e) q[e] = fast_index<FB_T>(c[e], R, r, near);
+        for (int e = 0; e < V; ++e) q[e] = fast_index<FB_T>(c[ch * V + e], R, r, near);
         if (near) {
 #pragma unroll
           for (int e = 0; e < V; ++e) {
             bool nr = false;
-            fast_index<FB_T>(c[e], R, r, nr);
-            if (nr) q[e] = bin_exact_out(c[e], n, r, r);
+            fast_index<FB_T>(c[ch * V + e], R, r, nr);
+            if (nr) q[e] = bin_exact_out(c[ch * V + e], n, r, r);
           }
         }
       }
-      if (valid) {
-        if (vec && k0 + V <= kept) {
-          uint32_t w[4] = {0, 0, 0, 0};
+      if (vec && k0 + V <= kept) {
+        uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-          for (int e = 0; e < V; ++e) {
-            if constexpr (sizeof(IT) == 8) {
-              w[2 * e] = (uint32_t)q[e];
-              w[2 * e + 1] = (uint32_t)((unsigned long long)q[e] >> 32);
-            } else {
-              const uint32_t bits = (uint32_t)q[e] & (sizeof(IT) == 4 ? 0xffffffffu : ((1u << (8 * sizeof(IT))) - 1));
-              w[(e * sizeof(IT)) / 4] |= bits << ((e * sizeof(IT) * 8) % 32);
-            }
+        for (int e = 0; e < V; ++e) {
+          if constexpr (sizeof(IT) == 8) {
+            w[2 * e] = (uint32_t)q[e];
+            w[2 * e + 1] = (uint32_t)((unsigned long long)q[e] >> 32);
+          } else {
+            const uint32_t bits = (uint32_t)q[e] & (sizeof(IT) == 4 ? 0xffffffffu : ((1u << (8 * sizeof(IT))) - 1));
+            w[(e * sizeof(IT)) / 4] |= bits << ((e * sizeof(IT) * 8) % 32);
           }
-          __stcs(reinterpret_cast<uint4*>(out_idx + base + k0), make_uint4(w[0], w[1], w[2], w[3]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < V; ++e)
-            if (k0 + e < kept) out_idx[base + k0 + e] = (IT)q[e];
         }
+        __stcs(reinterpret_cast<uint4*>(out_idx + base + k0), make_uint4(w[0], w[1], w[2], w[3]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          if (k0 + e < kept) out_idx[base + k0 + e] = (IT)q[e];
       }
     }
   }
@@ -268,21 +268,35 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
                         int mode, void* out_max, void* out_idx, cudaStream_t s) {
   constexpr int V = 16 / sizeof(IT);
   const int kept = ga.kept;
-  int GS = 1;
-  while (GS < 32 && GS * V < kept) GS <<= 1;
+  const int vecs = (kept + V - 1) / V;  // chunks per block
+  // one lane per block for small blocks; otherwise spread over up to 32 lanes
+  int GS = 1, NCH = 1;
+  if (vecs <= 4) {
+    NCH = vecs <= 1 ? 1 : (vecs <= 2 ? 2 : 4);
+  } else {
+    while (GS < 32 && GS < vecs) GS <<= 1;
+    NCH = (vecs + GS - 1) / GS;
+    if (NCH > 4) { set_error("add: kept block too large (%d indices)", kept); return BZ_E_UNSUPPORTED; }
+    NCH = NCH <= 1 ? 1 : (NCH <= 2 ? 2 : 4);
+  }
   const bool vec = ((kept * sizeof(IT)) % 16 == 0) &&
                    !(((uintptr_t)a_idx | (uintptr_t)out_idx | (mode == 0 ? (uintptr_t)b_idx : 0)) & 15);
   const int64_t threads = ga.nblocks * GS;
   const int grid = grid_for(threads, 256, 8);
-#define BZ_GS(G)                                                                              \
-  case G:                                                                                     \
-    k_add<IT, G><<<grid, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind, gb.float_kind,         \
-                                      ga.float_kind, a_max, (const IT*)a_idx, b_max,          \
-                                      (const IT*)b_idx, subtract, shift, mode, out_max,       \
-                                      (IT*)out_idx, vec);                                     \
+#define BZ_LAUNCH(G, N)                                                                      \
+  k_add<IT, G, N><<<grid, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind, gb.float_kind,       \
+                                       ga.float_kind, a_max, (const IT*)a_idx, b_max,        \
+                                       (const IT*)b_idx, subtract, shift, mode, out_max,     \
+                                       (IT*)out_idx, vec)
+#define BZ_GS(G)                                   \
+  case G:                                          \
+    if (NCH == 1) BZ_LAUNCH(G, 1);                 \
+    else if (NCH == 2) BZ_LAUNCH(G, 2);            \
+    else BZ_LAUNCH(G, 4);                          \
     break;
   switch (GS) { BZ_GS(1) BZ_GS(2) BZ_GS(4) BZ_GS(8) BZ_GS(16) BZ_GS(32) }
 #undef BZ_GS
+#undef BZ_LAUNCH
   return check_launch("add");
 }
 
