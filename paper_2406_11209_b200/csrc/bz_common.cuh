@@ -196,6 +196,82 @@ __device__ __forceinline__ int fast_index(double c, double R, double rr, bool& n
   return (int)idx;
 }
 
+// 32-bit fixed-point variant for I8 / I16: no 64-bit integer ops; `nacc`
+// collects a "near one half" flag; CLAMP only where the stored maximum can
+// round far enough below the true maximum for |v| to reach r + 1/2.
+template <typename IT, bool CLAMP>
+__device__ __forceinline__ int fast_index32(double c, double R, int ir, unsigned& nacc) {
+  using FB = FastBin<IT>;
+  static_assert(sizeof(typename FB::Fix) == 4, "32-bit fixed point only");
+  constexpr double MAGIC = 1.5 * (double)(1ll << (52 - FB::K));
+  constexpr unsigned HALF = 1u << (FB::K - 1);
+  constexpr unsigned MASK = (1u << FB::K) - 1;
+  const int fx = __double2loint(__fma_rn(c, R, MAGIC));
+  nacc |= (unsigned)((((unsigned)fx & MASK) - (HALF - FB::W)) <= 2u * FB::W);
+  int idx = (fx + (int)HALF) >> FB::K;
+  if (CLAMP) idx = min(max(idx, -ir), ir);
+  return idx;
+}
+
+// Per-block binning context: everything the exact reference binning
+// rint(fl(C / N) * r) (codec.py:272-277) needs, without IEEE division calls.
+//  * N = 0, inf or NaN: every C / N is non-finite or 0 -> every index is 0.
+//  * otherwise C / N = fl(C*s / (N*s)) with s a power of two lifting a tiny N
+//    into the normal range, computed by Markstein's correction with the
+//    correctly rounded reciprocal y = RN(1 / (N*s)).
+//  * R ~ r / N feeds the fixed-point fast path (its error is covered by the
+//    near-half window, so it need not be correctly rounded).
+struct BinCtx {
+  double R, ns, y, s;
+  bool zero;  // all indices are 0
+  bool fast;  // fast fixed-point path valid (N normal, not tiny)
+};
+
+__device__ __forceinline__ BinCtx bin_ctx(double n, double rr) {
+  BinCtx b;
+  b.zero = !(n > 0.0) || !(n <= 1.7976931348623157e308);
+  b.s = n < 0x1p-900 ? 0x1p+600 : 1.0;
+  b.ns = b.zero ? 1.0 : n * b.s;
+  b.y = __drcp_rn(b.ns);
+  b.R = rr * b.y * b.s;
+  b.fast = !b.zero && n >= 0x1p-900;
+  return b;
+}
+
+__device__ __forceinline__ long long bin_exact_ctx(double c, const BinCtx& b, double rr,
+                                                   double bound) {
+  if (b.zero) return 0;
+  double q = div_const(c * b.s, b.ns, b.y);
+  if (!isfinite(q)) q = 0.0;
+  double v = rint(__dmul_rn(q, rr));
+  v = fmin(fmax(v, -bound), bound);
+  return (long long)v;
+}
+
+// pack 16 bytes of indices (I8: 16 values, I16: 8 values) with PRMT
+template <typename IT>
+__device__ __forceinline__ uint4 pack16(const int* q) {
+  uint4 w;
+  if constexpr (sizeof(IT) == 1) {
+    unsigned o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const unsigned lo = __byte_perm((unsigned)q[4 * k], (unsigned)q[4 * k + 1], 0x0040);
+      const unsigned hi = __byte_perm((unsigned)q[4 * k + 2], (unsigned)q[4 * k + 3], 0x0040);
+      o[k] = __byte_perm(lo, hi, 0x5410);
+    }
+    w = make_uint4(o[0], o[1], o[2], o[3]);
+  } else if constexpr (sizeof(IT) == 2) {
+    w = make_uint4(__byte_perm((unsigned)q[0], (unsigned)q[1], 0x5410),
+                   __byte_perm((unsigned)q[2], (unsigned)q[3], 0x5410),
+                   __byte_perm((unsigned)q[4], (unsigned)q[5], 0x5410),
+                   __byte_perm((unsigned)q[6], (unsigned)q[7], 0x5410));
+  } else {
+    w = make_uint4((unsigned)q[0], (unsigned)q[1], (unsigned)q[2], (unsigned)q[3]);
+  }
+  return w;
+}
+
 // ------------------------------------------------------------ descriptors --
 struct Geo {  // device-side copy of the layout geometry
   int ndim;

@@ -114,26 +114,57 @@ __device__ __forceinline__ void slice_coords(int o, int (&c)[4]) {
   }
 }
 
-// write slice (P,Q) of thread o into the block's canonical smem region
+// write slice (P,Q) of thread o into the block's canonical smem region.
+// When Q is the last axis, element pairs (j, j+1) are adjacent and move as
+// 16-byte accesses; the XOR swizzle then works on 16-byte units (`swz` is
+// even), so 8 lanes with consecutive block slots hit 8 distinct bank groups.
 template <int D, int E, int P, int Q>
 __device__ __forceinline__ void slice_store(double* blk, int swz, int o, const double* v) {
   const int base = slice_base<D, E, P, Q>(o);
+  if constexpr (Q == D - 1 && E % 2 == 0) {
 #pragma unroll
-  for (int i = 0; i < E; ++i)
+    for (int i = 0; i < E; ++i)
 #pragma unroll
-    for (int j = 0; j < E; ++j)
-      blk[(base + i * axis_stride<D, E>(P) + j * axis_stride<D, E>(Q)) ^ swz] = v[i * E + j];
+      for (int j = 0; j < E; j += 2)
+        *reinterpret_cast<double2*>(blk + ((base + i * axis_stride<D, E>(P) + j) ^ (swz & ~1))) =
+            (swz & 1) ? make_double2(v[i * E + j + 1], v[i * E + j])
+                      : make_double2(v[i * E + j], v[i * E + j + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+#pragma unroll
+      for (int j = 0; j < E; ++j)
+        blk[(base + i * axis_stride<D, E>(P) + j * axis_stride<D, E>(Q)) ^ swz] = v[i * E + j];
+  }
 }
 
 template <int D, int E, int P, int Q>
 __device__ __forceinline__ void slice_load(const double* blk, int swz, int o, double* v) {
   const int base = slice_base<D, E, P, Q>(o);
+  if constexpr (Q == D - 1 && E % 2 == 0) {
 #pragma unroll
-  for (int i = 0; i < E; ++i)
+    for (int i = 0; i < E; ++i)
 #pragma unroll
-    for (int j = 0; j < E; ++j)
-      v[i * E + j] = blk[(base + i * axis_stride<D, E>(P) + j * axis_stride<D, E>(Q)) ^ swz];
+      for (int j = 0; j < E; j += 2) {
+        const double2 w =
+            *reinterpret_cast<const double2*>(blk + ((base + i * axis_stride<D, E>(P) + j) ^ (swz & ~1)));
+        v[i * E + j] = (swz & 1) ? w.y : w.x;
+        v[i * E + j + 1] = (swz & 1) ? w.x : w.y;
+      }
+  } else {
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+#pragma unroll
+      for (int j = 0; j < E; ++j)
+        v[i * E + j] = blk[(base + i * axis_stride<D, E>(P) + j * axis_stride<D, E>(Q)) ^ swz];
+  }
 }
+
+// swizzle key for block slot lb: bits 1-3 spread 16-byte units over the 8
+// bank groups (conflict-free 128-bit phases of 8 lanes), bit 0 makes 16
+// consecutive slots distinct for 64-bit accesses; 16-byte pair accesses
+// apply bit 0 as an in-pair swap
+__device__ __forceinline__ int slot_swizzle(int lb) { return ((lb & 7) << 1) | ((lb >> 3) & 1); }
 
 // ------------------------------------------------- reference-exact lines --
 // forward: C[k] = fma chain over n of x[n] * H[n][k];  inverse: y[n] = fma

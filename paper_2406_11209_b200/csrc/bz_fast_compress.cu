@@ -17,6 +17,8 @@
 #include "bz_fast.cuh"
 #include "bz_kernels.cuh"
 
+#include <cstdlib>
+
 namespace bz {
 
 // exact reference binning, out of line: reached for ~1e-5 of coefficients
@@ -56,7 +58,7 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
   const int lb = t % BPC;
   const int o = t / BPC;
   const double rr = radius_f64(sizeof(IT) == 1 ? BZ_I8 : (sizeof(IT) == 2 ? BZ_I16 : BZ_I32));
-  const int swz = lb & 15;
+  const int swz = slot_swizzle(lb);
   double* blk = xs + lb * BS;
 
   // per-thread private prefetch stage: the next tile's slice rows arrive by
@@ -186,17 +188,36 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
     if (f.full_mask) {
       if (valid) {
         IT* dst = indices + b * (int64_t)BS + o * NIN;
-        if constexpr ((NIN * sizeof(IT)) % 16 == 0) {
+        if constexpr ((NIN * sizeof(IT)) % 16 == 0 && sizeof(IT) <= 2) {
+          constexpr int PER = 16 / sizeof(IT);
+          // v <= r(1+2^-24) for F32/F64 maxima: rounding cannot exceed r
+          constexpr bool CLAMP = !(FK == BZ_F32 || FK == BZ_F64);
+          const int ir = (int)rr;
+#pragma unroll
+          for (int cch = 0; cch < NIN / PER; ++cch) {
+            int q[PER];
+            unsigned nacc = 0;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) q[e] = fast_index32<IT, CLAMP>(v[cch * PER + e], R, ir, nacc);
+            if (nacc | special) {  // rare: exact reference arithmetic where needed
+#pragma unroll
+              for (int e = 0; e < PER; ++e) {
+                unsigned nr = 0;
+                fast_index32<IT, CLAMP>(v[cch * PER + e], R, ir, nr);
+                if (nr | special) q[e] = bin_exact_call(v[cch * PER + e], n, rr);
+              }
+            }
+            __stcs(reinterpret_cast<uint4*>(dst) + cch, pack16<IT>(q));
+          }
+        } else if constexpr ((NIN * sizeof(IT)) % 16 == 0) {
           constexpr int PER = 16 / sizeof(IT);
 #pragma unroll
           for (int cch = 0; cch < NIN / PER; ++cch) {
-            uint32_t w[4] = {0, 0, 0, 0};
+            int q[PER];
 #pragma unroll
-            for (int e = 0; e < PER; ++e) {
-              const int qv = special ? bin_exact_call(v[cch * PER + e], n, rr) : bin_one<IT>(v[cch * PER + e], R, n, rr);
-              w[(e * sizeof(IT)) / 4] |= idx_bits<IT>(qv) << ((e * sizeof(IT) * 8) % 32);
-            }
-            __stcs(reinterpret_cast<uint4*>(dst) + cch, make_uint4(w[0], w[1], w[2], w[3]));
+            for (int e = 0; e < PER; ++e)
+              q[e] = special ? bin_exact_call(v[cch * PER + e], n, rr) : bin_one<IT>(v[cch * PER + e], R, n, rr);
+            __stcs(reinterpret_cast<uint4*>(dst) + cch, pack16<IT>(q));
           }
         } else {
 #pragma unroll
@@ -295,6 +316,7 @@ bool fast_supported(const Geo& g, int x_kind) {
 int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s) {
   int E;
   uniform_block(g, E);
+  if (g.ndim == 3 && !getenv("BZC_B200_SLICE3")) return launch_line3_compress(g, x, maxima, indices, s);
 #define BZ_CASE(DD, EE) \
   if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, x, maxima, indices, s);
   BZ_CASE(1, 4) BZ_CASE(1, 8) BZ_CASE(2, 4) BZ_CASE(2, 8) BZ_CASE(3, 4) BZ_CASE(3, 8)

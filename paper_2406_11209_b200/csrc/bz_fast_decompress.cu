@@ -11,6 +11,8 @@
 #include "bz_fast.cuh"
 #include "bz_kernels.cuh"
 
+#include <cstdlib>
+
 namespace bz {
 
 template <typename IT, int N>
@@ -55,7 +57,7 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
   const double rr = radius_f64(sizeof(IT) == 1 ? BZ_I8 : (sizeof(IT) == 2 ? BZ_I16 : BZ_I32));
   const double rinv = 1.0 / rr;
   const double nsafe = 1.7976931348623157e308 / (rr * TL::BS * 4.0);
-  const int swz = lb & 15;
+  const int swz = slot_swizzle(lb);
   double* blk = xs + lb * BS;
   const bool stage_in = TL::EXCH || !f.full_mask;
 
@@ -242,6 +244,8 @@ bool fast_decompress_supported(const Geo& g, int out_kind) {
 int launch_fast_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s) {
   const int E = g.block[0];
+  if (g.ndim == 3 && !getenv("BZC_B200_SLICE3"))
+    return launch_line3_decompress(g, maxima, indices, out, out_kind, s);
 #define BZ_CASE(DD, EE) \
   if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, maxima, indices, out, out_kind, s);
   BZ_CASE(1, 4) BZ_CASE(1, 8) BZ_CASE(2, 4) BZ_CASE(2, 8) BZ_CASE(3, 4) BZ_CASE(3, 8)

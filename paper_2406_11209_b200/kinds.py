@@ -190,7 +190,8 @@ def as_device_tensor(values, device=None) -> torch.Tensor:
         t = values
         if t.dtype not in _KIND_OF_TORCH:
             t = t.to(torch.float64)
-        return t.to(dev).contiguous()
+        # pinned host memory: asynchronous H2D on the current stream
+        return t.to(dev, non_blocking=(not t.is_cuda and t.is_pinned())).contiguous()
     arr = np.asarray(values)
     if arr.dtype == np.float32:
         t = torch.from_numpy(np.ascontiguousarray(arr))

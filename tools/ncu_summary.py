@@ -30,3 +30,24 @@ if __name__ == "__main__":
     for p in sys.argv[1:]:
         print("==", p)
         print(summarise(p))
+
+
+def traffic_from_raw(path):
+    """{kernel name: dram bytes (read+write) per launch, median over launches}."""
+    import statistics
+
+    rows = list(csv.reader(open(path)))
+    hdr = rows[0]
+    ix = {h: i for i, h in enumerate(hdr)}
+    rd = ix.get("dram__bytes_read.sum")
+    wr = ix.get("dram__bytes_write.sum")
+    per = collections.defaultdict(list)
+    for r in rows[2:]:  # row 1 holds units
+        if len(r) < len(hdr) or rd is None:
+            continue
+        try:
+            per[r[ix["Kernel Name"]].split("(")[0]].append(
+                float(r[rd].replace(",", "")) + float(r[wr].replace(",", "")))
+        except ValueError:
+            continue
+    return {k: statistics.median(v) for k, v in per.items()}
