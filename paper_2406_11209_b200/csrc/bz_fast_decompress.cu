@@ -54,6 +54,12 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
   const int t = threadIdx.x;
   const int lb = t % BPC;
   const int o = t / BPC;
+  // rank table (position -> kept rank) in shared memory for pruned masks
+  int16_t* rks = reinterpret_cast<int16_t*>(stages + 2 * stage_bytes);
+  if (!f.full_mask) {
+    for (int i = t; i < BS; i += NT) rks[i] = (int16_t)f.rank[i];
+    __syncthreads();
+  }
   const double rr = radius_f64(sizeof(IT) == 1 ? BZ_I8 : (sizeof(IT) == 2 ? BZ_I16 : BZ_I32));
   const double rinv = 1.0 / rr;
   const double nsafe = 1.7976931348623157e308 / (rr * TL::BS * 4.0);
@@ -103,7 +109,7 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
 #pragma unroll
         for (int j = 0; j < E; ++j) {
           const int pos = base + i * axis_stride<D, E>(LP) * (D >= 2) + j * axis_stride<D, E>(LQ);
-          const int rk = f.full_mask ? pos : f.rank[pos];
+          const int rk = f.full_mask ? pos : rks[pos];
           v[i * E + j] = (valid && rk >= 0) ? (double)st[lb * f.kept + rk] : 0.0;
         }
     } else {
@@ -203,7 +209,8 @@ static int launch_one(const Geo& g, const void* maxima, const void* indices, voi
   }
   size_t smem = (TL::EXCH ? (size_t)TL::BPC * TL::BS * sizeof(double) : 0) +
                 ((TL::EXCH || !p.f.full_mask)
-                     ? 2 * (((size_t)TL::BPC * g.kept * sizeof(IT) + 16 + 15) / 16 * 16) : 0);
+                     ? 2 * (((size_t)TL::BPC * g.kept * sizeof(IT) + 16 + 15) / 16 * 16) : 0) +
+                (p.f.full_mask ? 0 : (size_t)TL::BS * 2 + 16);
   auto kern = k_fast_decompress<D, E, IT, FK, TOut>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
@@ -244,7 +251,7 @@ bool fast_decompress_supported(const Geo& g, int out_kind) {
 int launch_fast_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s) {
   const int E = g.block[0];
-  if (g.ndim == 3 && !getenv("BZC_B200_SLICE3"))
+  if (g.ndim == 3 && getenv("BZC_B200_LINE3"))
     return launch_line3_decompress(g, maxima, indices, out, out_kind, s);
 #define BZ_CASE(DD, EE) \
   if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, maxima, indices, out, out_kind, s);

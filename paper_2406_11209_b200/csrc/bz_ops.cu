@@ -147,19 +147,33 @@ __device__ __forceinline__ double fn_product(long long f, const Scale& s) {
   return __dmul_rn((double)f, s.n);
 }
 
+// one chunk (16 bytes) of a block's kept indices as integers
+template <typename IT>
+__device__ __forceinline__ void unpack_chunk(const uint4& w, elem_t<IT> (&out)[16 / sizeof(IT)]) {
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int e = 0; e < 16 / (int)sizeof(IT); ++e) {
+    if constexpr (sizeof(IT) == 1) out[e] = (int8_t)(ws[e / 4] >> (8 * (e % 4)));
+    else if constexpr (sizeof(IT) == 2) out[e] = (int16_t)(ws[e / 2] >> (16 * (e % 2)));
+    else if constexpr (sizeof(IT) == 4) out[e] = (int32_t)ws[e];
+    else out[e] = (long long)(((unsigned long long)ws[2 * e + 1] << 32) | ws[2 * e]);
+  }
+}
+
 // mode 0: a + (+/-)b     mode 1: a + shift at the first coefficient (add_scalar)
 // A group of GS lanes handles one block; each lane keeps NCH chunks of V
 // coefficients in registers (GS*NCH*V >= kept), so the block is read once.
-template <typename IT, int GS, int NCH>
-__global__ void __launch_bounds__(256)
+// VEC: the kept indices of every block are whole 16-byte vectors -- the next
+// block's vectors and maxima are loaded before the current block computes.
+template <typename IT, int GS, int NCH, bool VEC>
+__global__ void __launch_bounds__(256, 3)
 k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
       const void* __restrict__ a_max, const IT* __restrict__ a_idx,
       const void* __restrict__ b_max, const IT* __restrict__ b_idx, int subtract,
-      double shift, int mode, void* __restrict__ out_max, IT* __restrict__ out_idx, bool vec) {
+      double shift, int mode, void* __restrict__ out_max, IT* __restrict__ out_idx) {
   constexpr int V = 16 / sizeof(IT);
   constexpr int L = NCH * V;  // coefficients per lane
   constexpr int IK = sizeof(IT) == 1 ? BZ_I8 : sizeof(IT) == 2 ? BZ_I16 : sizeof(IT) == 4 ? BZ_I32 : BZ_I64;
-  using FB_T = typename std::conditional<sizeof(IT) == 8, int32_t, IT>::type;
   const double r = radius_f64(IK), bound = clamp_bound_f64(IK);
   const double rinv = 1.0 / r;
   const int lane = threadIdx.x & 31;
@@ -167,10 +181,40 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
   const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1) << (lane - sub));
   const int64_t group = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GS;
   const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / GS;
+
+  // software pipeline (VEC): registers for the next block's raw data
+  uint4 pa[NCH], pb[NCH];
+  double pna = 0.0, pnb = 0.0;
+  auto fetch = [&](int64_t b) {
+    if (b < nblocks) {
+      const int64_t base = b * (int64_t)kept;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int k0 = (ch * GS + sub) * V;
+        pa[ch] = k0 < kept ? __ldcs(reinterpret_cast<const uint4*>(a_idx + base + k0)) : make_uint4(0, 0, 0, 0);
+        pb[ch] = (mode == 0 && k0 < kept) ? __ldcs(reinterpret_cast<const uint4*>(b_idx + base + k0))
+                                          : make_uint4(0, 0, 0, 0);
+      }
+      pna = load_kind_rt(a_max, b, fk_a);
+      pnb = mode == 0 ? load_kind_rt(b_max, b, fk_b) : 0.0;
+    }
+  };
+  if (VEC) fetch(group);
+
   for (int64_t b = group; b < nblocks; b += ngroups) {
     const int64_t base = b * (int64_t)kept;
-    const double na = load_kind_rt(a_max, b, fk_a);
-    const double nb = mode == 0 ? load_kind_rt(b_max, b, fk_b) : 0.0;
+    double na, nb;
+    uint4 ca[NCH], cb[NCH];
+    if (VEC) {
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) { ca[ch] = pa[ch]; cb[ch] = pb[ch]; }
+      na = pna;
+      nb = pnb;
+      fetch(b + ngroups);  // next block's loads are in flight during this block
+    } else {
+      na = load_kind_rt(a_max, b, fk_a);
+      nb = mode == 0 ? load_kind_rt(b_max, b, fk_b) : 0.0;
+    }
     const Scale sa = make_scale(na, fk_a), sb = make_scale(nb, fk_b);
     const bool safe = na >= 0x1p-900 && na <= 0x1p+900 &&
                       (mode != 0 || (nb >= 0x1p-900 && nb <= 0x1p+900));
@@ -180,26 +224,31 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
     for (int ch = 0; ch < NCH; ++ch) {
       const int k0 = (ch * GS + sub) * V;
       elem_t<IT> fa[V], fb[V];
-      load_chunk<IT>(a_idx, base, k0, kept, vec, fa);
-      if (mode == 0) load_chunk<IT>(b_idx, base, k0, kept, vec, fb);
+      if (VEC) {
+        unpack_chunk<IT>(ca[ch], fa);
+        unpack_chunk<IT>(cb[ch], fb);
+      } else {
+        load_chunk<IT>(a_idx, base, k0, kept, false, fa);
+        if (mode == 0) load_chunk<IT>(b_idx, base, k0, kept, false, fb);
+      }
 #pragma unroll
       for (int e = 0; e < V; ++e) {
         double cc;
         if (safe) {
-          const double ca = div_const(fn_product(fa[e], sa), r, rinv);
+          const double xa = div_const(fn_product(fa[e], sa), r, rinv);
           if (mode == 0) {
             const elem_t<IT> fbv = subtract ? -fb[e] : fb[e];
-            cc = __dadd_rn(ca, div_const(fn_product(fbv, sb), r, rinv));
+            cc = __dadd_rn(xa, div_const(fn_product(fbv, sb), r, rinv));
           } else {
-            cc = (k0 + e == 0) ? __dadd_rn(ca, shift) : ca;
+            cc = (k0 + e == 0) ? __dadd_rn(xa, shift) : xa;
           }
         } else {
-          const double ca = spec_coeff_slow((double)fa[e], na, r);
+          const double xa = spec_coeff_slow((double)fa[e], na, r);
           if (mode == 0) {
             const double fbv = subtract ? -(double)fb[e] : (double)fb[e];
-            cc = __dadd_rn(ca, spec_coeff_slow(fbv, nb, r));
+            cc = __dadd_rn(xa, spec_coeff_slow(fbv, nb, r));
           } else {
-            cc = (k0 + e == 0) ? __dadd_rn(ca, shift) : ca;
+            cc = (k0 + e == 0) ? __dadd_rn(xa, shift) : xa;
           }
         }
         c[ch * V + e] = cc;
@@ -217,46 +266,58 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
     const double mx = __longlong_as_double((long long)key);  // NaN-propagating via bit order
     const double n = round_to_kind_rt(mx, fk_out);
     if (sub == 0) store_kind_rt(out_max, b, n, fk_out);
-    const bool special = sizeof(IT) == 8 || !(mx <= 1.7976931348623157e308) ||
-                         !(n >= 0x1p-1000) || (mx > n * 1.00390625);
-    const double R = special ? 0.0 : __ddiv_rn(r, n);
+    const BinCtx bc = bin_ctx(n, r);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       const int k0 = (ch * GS + sub) * V;
-      long long q[V];
-      if (special) {
+      int q[V];
+      if constexpr (sizeof(IT) <= 2) {
+        unsigned nacc = 0;
 #pragma unroll
-        for (int e = 0; e < V; ++e) q[e] = bin_exact_out(c[ch * V + e], n, r, bound);
-      } else {
-        bool near = false;
-#pragma unroll
-        for (int e = 0; e < V; ++e) q[e] = fast_index<FB_T>(c[ch * V + e], R, r, near);
-        if (near) {
+        for (int e = 0; e < V; ++e) q[e] = fast_index32<IT, true>(c[ch * V + e], bc.R, (int)r, nacc);
+        if (nacc | !bc.fast) {
 #pragma unroll
           for (int e = 0; e < V; ++e) {
-            bool nr = false;
-            fast_index<FB_T>(c[ch * V + e], R, r, nr);
-            if (nr) q[e] = bin_exact_out(c[ch * V + e], n, r, r);
+            unsigned nr = 0;
+            fast_index32<IT, true>(c[ch * V + e], bc.R, (int)r, nr);
+            if (nr | !bc.fast) q[e] = (int)bin_exact_ctx(c[ch * V + e], bc, r, r);
           }
         }
       }
-      if (vec && k0 + V <= kept) {
-        uint32_t w[4] = {0, 0, 0, 0};
+      long long q64[V];
+      if constexpr (sizeof(IT) > 2) {
 #pragma unroll
         for (int e = 0; e < V; ++e) {
-          if constexpr (sizeof(IT) == 8) {
-            w[2 * e] = (uint32_t)q[e];
-            w[2 * e + 1] = (uint32_t)((unsigned long long)q[e] >> 32);
-          } else {
-            const uint32_t bits = (uint32_t)q[e] & (sizeof(IT) == 4 ? 0xffffffffu : ((1u << (8 * sizeof(IT))) - 1));
-            w[(e * sizeof(IT)) / 4] |= bits << ((e * sizeof(IT) * 8) % 32);
+          bool nr = false;
+          if constexpr (sizeof(IT) == 4) q64[e] = bc.fast ? fast_index<int32_t>(c[ch * V + e], bc.R, r, nr) : 0;
+          else q64[e] = 0;
+          if (nr || !bc.fast || sizeof(IT) == 8) q64[e] = bin_exact_ctx(c[ch * V + e], bc, r, bound);
+        }
+      }
+      if (VEC && k0 < kept) {
+        if constexpr (sizeof(IT) <= 2) {
+          __stcs(reinterpret_cast<uint4*>(out_idx + base + k0), pack16<IT>(q));
+        } else {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            if constexpr (sizeof(IT) == 8) {
+              w[2 * e] = (uint32_t)q64[e];
+              w[2 * e + 1] = (uint32_t)((unsigned long long)q64[e] >> 32);
+            } else {
+              w[e] = (uint32_t)q64[e];
+            }
+          }
+          __stcs(reinterpret_cast<uint4*>(out_idx + base + k0), make_uint4(w[0], w[1], w[2], w[3]));
+        }
+      } else if (!VEC) {
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          if (k0 + e < kept) {
+            if constexpr (sizeof(IT) <= 2) out_idx[base + k0 + e] = (IT)q[e];
+            else out_idx[base + k0 + e] = (IT)q64[e];
           }
         }
-        __stcs(reinterpret_cast<uint4*>(out_idx + base + k0), make_uint4(w[0], w[1], w[2], w[3]));
-      } else {
-#pragma unroll
-        for (int e = 0; e < V; ++e)
-          if (k0 + e < kept) out_idx[base + k0 + e] = (IT)q[e];
       }
     }
   }
@@ -282,12 +343,20 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
   const bool vec = ((kept * sizeof(IT)) % 16 == 0) &&
                    !(((uintptr_t)a_idx | (uintptr_t)out_idx | (mode == 0 ? (uintptr_t)b_idx : 0)) & 15);
   const int64_t threads = ga.nblocks * GS;
-  const int grid = grid_for(threads, 256, 8);
-#define BZ_LAUNCH(G, N)                                                                      \
-  k_add<IT, G, N><<<grid, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind, gb.float_kind,       \
-                                       ga.float_kind, a_max, (const IT*)a_idx, b_max,        \
-                                       (const IT*)b_idx, subtract, shift, mode, out_max,     \
-                                       (IT*)out_idx, vec)
+  const int grid = grid_for(threads, 256, 3);  // persistent: 3 CTAs per SM
+#define BZ_LAUNCH(G, N)                                                                         \
+  do {                                                                                          \
+    if (vec)                                                                                    \
+      k_add<IT, G, N, true><<<grid, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind, gb.float_kind, \
+                                                ga.float_kind, a_max, (const IT*)a_idx, b_max,  \
+                                                (const IT*)b_idx, subtract, shift, mode,        \
+                                                out_max, (IT*)out_idx);                         \
+    else                                                                                        \
+      k_add<IT, G, N, false><<<grid, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind,               \
+                                                 gb.float_kind, ga.float_kind, a_max,           \
+                                                 (const IT*)a_idx, b_max, (const IT*)b_idx,     \
+                                                 subtract, shift, mode, out_max, (IT*)out_idx); \
+  } while (0)
 #define BZ_GS(G)                                   \
   case G:                                          \
     if (NCH == 1) BZ_LAUNCH(G, 1);                 \
