@@ -220,21 +220,24 @@ __device__ __forceinline__ int fast_index32(double c, double R, int ir, unsigned
 //    into the normal range, computed by Markstein's correction with the
 //    correctly rounded reciprocal y = RN(1 / (N*s)).
 //  * R ~ r / N feeds the fixed-point fast path (its error is covered by the
-//    near-half window, so it need not be correctly rounded).
+//    near-half window, so it need not be correctly rounded); mx is the true
+//    block maximum the stored N was rounded from.
 struct BinCtx {
   double R, ns, y, s;
   bool zero;  // all indices are 0
   bool fast;  // fast fixed-point path valid (N normal, not tiny)
 };
 
-__device__ __forceinline__ BinCtx bin_ctx(double n, double rr) {
+__device__ __forceinline__ BinCtx bin_ctx(double n, double rr, double mx) {
   BinCtx b;
   b.zero = !(n > 0.0) || !(n <= 1.7976931348623157e308);
   b.s = n < 0x1p-900 ? 0x1p+600 : 1.0;
   b.ns = b.zero ? 1.0 : n * b.s;
   b.y = __drcp_rn(b.ns);
   b.R = rr * b.y * b.s;
-  b.fast = !b.zero && n >= 0x1p-900;
+  // fast path: |v| <= r(1+2^-8) keeps the fixed point in range (a stored
+  // maximum rounded far below the true one -- narrow-kind subnormals -- is not)
+  b.fast = !b.zero && n >= 0x1p-900 && mx <= n * 1.00390625;
   return b;
 }
 

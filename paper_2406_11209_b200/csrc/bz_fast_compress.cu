@@ -197,11 +197,23 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
     }
     const double mx = __longlong_as_double((long long)key);
     const double n = round_to_kind<FK>(mx);
-    const bool special = !(mx <= 1.7976931348623157e308) || !(n >= 0x1p-1000) ||
-                         (mx > n * 1.00390625);
-    const double R = special ? 0.0 : __ddiv_rn(rr, n);
-
+    const BinCtx bc = bin_ctx(n, rr, mx);
     if (valid && o == 0) store_kind<FK>(maxima, b, n);
+    // v <= r(1+2^-24) for F32/F64 maxima: rounding cannot exceed r
+    constexpr bool CLAMP = !(FK == BZ_F32 || FK == BZ_F64);
+    const int ir = (int)rr;
+    // exact reference index of coefficient q (near-half fraction / non-fast block)
+    auto bin_q = [&](double c) -> int {
+      if constexpr (sizeof(IT) <= 2) {
+        unsigned nr = 0;
+        const int qv = fast_index32<IT, CLAMP>(c, bc.R, ir, nr);
+        return (nr | !bc.fast) ? (int)bin_exact_ctx(c, bc, rr, rr) : qv;
+      } else {
+        bool nr = false;
+        const int qv = bc.fast ? fast_index<IT>(c, bc.R, rr, nr) : 0;
+        return (nr || !bc.fast) ? (int)bin_exact_ctx(c, bc, rr, rr) : qv;
+      }
+    };
 
     // ---- bin + store kept indices
     if (f.full_mask) {
@@ -209,22 +221,15 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
         IT* dst = indices + b * (int64_t)BS + o * NIN;
         if constexpr ((NIN * sizeof(IT)) % 16 == 0 && sizeof(IT) <= 2) {
           constexpr int PER = 16 / sizeof(IT);
-          // v <= r(1+2^-24) for F32/F64 maxima: rounding cannot exceed r
-          constexpr bool CLAMP = !(FK == BZ_F32 || FK == BZ_F64);
-          const int ir = (int)rr;
 #pragma unroll
           for (int cch = 0; cch < NIN / PER; ++cch) {
             int q[PER];
             unsigned nacc = 0;
 #pragma unroll
-            for (int e = 0; e < PER; ++e) q[e] = fast_index32<IT, CLAMP>(v[cch * PER + e], R, ir, nacc);
-            if (nacc | special) {  // rare: exact reference arithmetic where needed
+            for (int e = 0; e < PER; ++e) q[e] = fast_index32<IT, CLAMP>(v[cch * PER + e], bc.R, ir, nacc);
+            if (nacc | !bc.fast) {  // rare: exact reference arithmetic where needed
 #pragma unroll
-              for (int e = 0; e < PER; ++e) {
-                unsigned nr = 0;
-                fast_index32<IT, CLAMP>(v[cch * PER + e], R, ir, nr);
-                if (nr | special) q[e] = bin_exact_call(v[cch * PER + e], n, rr);
-              }
+              for (int e = 0; e < PER; ++e) q[e] = bin_q(v[cch * PER + e]);
             }
             __stcs(reinterpret_cast<uint4*>(dst) + cch, pack16<IT>(q));
           }
@@ -234,13 +239,12 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
           for (int cch = 0; cch < NIN / PER; ++cch) {
             int q[PER];
 #pragma unroll
-            for (int e = 0; e < PER; ++e)
-              q[e] = special ? bin_exact_call(v[cch * PER + e], n, rr) : bin_one<IT>(v[cch * PER + e], R, n, rr);
+            for (int e = 0; e < PER; ++e) q[e] = bin_q(v[cch * PER + e]);
             __stcs(reinterpret_cast<uint4*>(dst) + cch, pack16<IT>(q));
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < NIN; ++q) dst[q] = (IT)(special ? bin_exact_call(v[q], n, rr) : bin_one<IT>(v[q], R, n, rr));
+          for (int q = 0; q < NIN; ++q) dst[q] = (IT)bin_q(v[q]);
         }
       }
     } else {
@@ -252,7 +256,7 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
 #pragma unroll
         for (int q = 0; q < NIN; ++q) {
           const int rk = rks[o * NIN + q];
-          if (rk >= 0) st[lb * f.kept + rk] = (IT)(special ? bin_exact_call(v[q], n, rr) : bin_one<IT>(v[q], R, n, rr));
+          if (rk >= 0) st[lb * f.kept + rk] = (IT)bin_q(v[q]);
         }
       }
       __syncthreads();
@@ -337,6 +341,8 @@ int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indice
   int E;
   uniform_block(g, E);
   if (g.ndim == 3 && getenv("BZC_B200_LINE3")) return launch_line3_compress(g, x, maxima, indices, s);
+  if (g.ndim == 3 && E == 8 && !getenv("BZC_B200_SLICE3"))
+    return launch_half3_compress(g, x, maxima, indices, s);
 #define BZ_CASE(DD, EE) \
   if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, x, maxima, indices, s);
   BZ_CASE(1, 4) BZ_CASE(1, 8) BZ_CASE(2, 4) BZ_CASE(2, 8) BZ_CASE(3, 4) BZ_CASE(3, 8)

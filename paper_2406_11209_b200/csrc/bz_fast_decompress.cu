@@ -253,6 +253,8 @@ int launch_fast_decompress(const Geo& g, const void* maxima, const void* indices
   const int E = g.block[0];
   if (g.ndim == 3 && getenv("BZC_B200_LINE3"))
     return launch_line3_decompress(g, maxima, indices, out, out_kind, s);
+  if (g.ndim == 3 && E == 8 && !getenv("BZC_B200_SLICE3"))
+    return launch_half3_decompress(g, maxima, indices, out, out_kind, s);
 #define BZ_CASE(DD, EE) \
   if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, maxima, indices, out, out_kind, s);
   BZ_CASE(1, 4) BZ_CASE(1, 8) BZ_CASE(2, 4) BZ_CASE(2, 8) BZ_CASE(3, 4) BZ_CASE(3, 8)

@@ -136,7 +136,7 @@ k_line3_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict
     }
     const double mx = __longlong_as_double((long long)key);
     const double n = round_to_kind<FK>(mx);
-    const BinCtx bc = bin_ctx(n, rr);
+    const BinCtx bc = bin_ctx(n, rr, mx);
     if (valid && l == 0) store_kind<FK>(maxima, b, n);
 
     // ---- bin the thread's E coefficients (exact reference rounding)

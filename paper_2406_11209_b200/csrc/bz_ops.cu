@@ -266,7 +266,7 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
     const double mx = __longlong_as_double((long long)key);  // NaN-propagating via bit order
     const double n = round_to_kind_rt(mx, fk_out);
     if (sub == 0) store_kind_rt(out_max, b, n, fk_out);
-    const BinCtx bc = bin_ctx(n, r);
+    const BinCtx bc = bin_ctx(n, r, mx);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       const int k0 = (ch * GS + sub) * V;

@@ -261,12 +261,29 @@ def moments_record(a: CompressedArray, b: CompressedArray | None = None, *,
     return rec
 
 
+_HOST_REC: dict = {}
+
+
+def record_to_host(rec: torch.Tensor) -> np.ndarray:
+    """Copy a device record through a pinned buffer, waiting on the current
+    stream only (a pageable .cpu() copy would stall other streams' copies)."""
+    dev = rec.device
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    h = _HOST_REC.get(key)
+    if h is None:
+        h = torch.empty(rec.numel(), dtype=rec.dtype, pin_memory=True)
+        _HOST_REC[key] = h
+    h.copy_(rec, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    return h.numpy().copy()
+
+
 def _reduce(a, b=None, *, dc_only=False) -> Record:
     """Record of the whole array (sharded arrays merge across ranks first)."""
     hook = getattr(a, "_reduce_record", None)
     if hook is not None:
         return hook(b, dc_only)
-    return Record.from_array(moments_record(a, b, dc_only=dc_only).cpu().numpy())
+    return Record.from_array(record_to_host(moments_record(a, b, dc_only=dc_only)))
 
 
 def _radius(a) -> float:
