@@ -228,6 +228,9 @@ struct BinCtx {
   bool fast;  // fast fixed-point path valid (N normal, not tiny)
 };
 
+// CLAMP = false callers (no index clamp in the fixed-point path) need |v| < r + 1/2,
+// i.e. a stored maximum within 2^-20 of the true one (F32 normal / F64 maxima).
+template <bool CLAMP = true>
 __device__ __forceinline__ BinCtx bin_ctx(double n, double rr, double mx) {
   BinCtx b;
   b.zero = !(n > 0.0) || !(n <= 1.7976931348623157e308);
@@ -237,7 +240,7 @@ __device__ __forceinline__ BinCtx bin_ctx(double n, double rr, double mx) {
   b.R = rr * b.y * b.s;
   // fast path: |v| <= r(1+2^-8) keeps the fixed point in range (a stored
   // maximum rounded far below the true one -- narrow-kind subnormals -- is not)
-  b.fast = !b.zero && n >= 0x1p-900 && mx <= n * 1.00390625;
+  b.fast = !b.zero && n >= 0x1p-900 && mx <= n * (CLAMP ? 1.00390625 : 1.00000095367431640625);
   return b;
 }
 

@@ -197,11 +197,11 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
     }
     const double mx = __longlong_as_double((long long)key);
     const double n = round_to_kind<FK>(mx);
-    const BinCtx bc = bin_ctx(n, rr, mx);
+    constexpr bool CLAMP = !(FK == BZ_F32 || FK == BZ_F64);
+    const BinCtx bc = bin_ctx<CLAMP>(n, rr, mx);
     if (valid && o == 0) store_kind<FK>(maxima, b, n);
     // v <= r(1+2^-24) for F32/F64 maxima: rounding cannot exceed r
-    constexpr bool CLAMP = !(FK == BZ_F32 || FK == BZ_F64);
-    const int ir = (int)rr;
+        const int ir = (int)rr;
     // exact reference index of coefficient q (near-half fraction / non-fast block)
     auto bin_q = [&](double c) -> int {
       if constexpr (sizeof(IT) <= 2) {

@@ -174,10 +174,10 @@ k_half3_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict
     }
     const double mx = __longlong_as_double((long long)mkey);
     const double n = round_to_kind<FK>(mx);
-    const BinCtx bc = bin_ctx(n, rr, mx);
-    if (valid && o == 0) store_kind<FK>(maxima, b, n);
     constexpr bool CLAMP = !(FK == BZ_F32 || FK == BZ_F64);
-    const int ir = (int)rr;
+    const BinCtx bc = bin_ctx<CLAMP>(n, rr, mx);
+    if (valid && o == 0) store_kind<FK>(maxima, b, n);
+        const int ir = (int)rr;
     auto bin_q = [&](double c) -> int {
       if constexpr (sizeof(IT) <= 2) {
         unsigned nr = 0;

@@ -136,14 +136,14 @@ k_line3_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict
     }
     const double mx = __longlong_as_double((long long)key);
     const double n = round_to_kind<FK>(mx);
-    const BinCtx bc = bin_ctx(n, rr, mx);
+    constexpr bool CLAMP = !(FK == BZ_F32 || FK == BZ_F64);
+    const BinCtx bc = bin_ctx<CLAMP>(n, rr, mx);
     if (valid && l == 0) store_kind<FK>(maxima, b, n);
 
     // ---- bin the thread's E coefficients (exact reference rounding)
     int q[E];
     if constexpr (sizeof(IT) <= 2) {
-      constexpr bool CLAMP = !(FK == BZ_F32 || FK == BZ_F64);
-      unsigned nacc = 0;
+            unsigned nacc = 0;
 #pragma unroll
       for (int k = 0; k < E; ++k) q[k] = fast_index32<IT, CLAMP>(out[k], bc.R, (int)rr, nacc);
       if (nacc | !bc.fast) {

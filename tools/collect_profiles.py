@@ -26,8 +26,10 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from ncu_summary import summarise  # noqa: E402
 
 OP_KERNELS = {  # bench op -> kernel name prefix
-    "compress": ("k_fast_compress", "k_line3_compress", "k_exact_compress"),
-    "decompress": ("k_fast_decompress", "k_line3_decompress", "k_exact_decompress"),
+    "compress": ("k_fast_compress", "k_half3_compress", "k_line3_compress", "k_exact_compress"),
+    "decompress": ("k_fast_decompress", "k_half3_decompress", "k_line3_decompress", "k_exact_decompress"),
+    "l2_norm": ("k_moments_vec", "k_moments_staged"),
+    "add": ("k_add",),
 }
 
 STALL_KEYS = [
