@@ -88,7 +88,12 @@ class DenseArray:
                     f"value buffer shaped {tuple(src.shape)} does not match shape {shape}"
                 )
             # a copy in the kind's dtype; narrowing is checked to be exact
-            t = _round_into(src, kind, check=(src.dtype != kind.torch_dtype))
+            if src.dtype == kind.torch_dtype:
+                fresh = not (isinstance(values, torch.Tensor) and values.is_cuda
+                             and values.data_ptr() == src.data_ptr())
+                t = src if fresh else src.clone()  # host data was already copied once
+            else:
+                t = _round_into(src, kind, check=True)
         object.__setattr__(self, "shape", shape)
         object.__setattr__(self, "kind", kind)
         object.__setattr__(self, "values", t)

@@ -36,6 +36,39 @@ __device__ __forceinline__ void load_indices_vec(const IT* __restrict__ src, dou
   }
 }
 
+// raw 16-byte chunks of one block's indices (register prefetch), unpacked later
+template <typename IT, int N>
+struct RawIdx {
+  static constexpr int C = (N * (int)sizeof(IT) + 15) / 16;
+  uint4 w[C];
+};
+
+template <typename IT, int N>
+__device__ __forceinline__ void load_raw(const IT* __restrict__ src, bool ok, RawIdx<IT, N>& r) {
+#pragma unroll
+  for (int c = 0; c < RawIdx<IT, N>::C; ++c)
+    r.w[c] = ok ? __ldcs(reinterpret_cast<const uint4*>(src) + c) : make_uint4(0, 0, 0, 0);
+}
+
+template <typename IT, int N>
+__device__ __forceinline__ void unpack_raw(const RawIdx<IT, N>& r, double* dst) {
+  constexpr int PER = 16 / sizeof(IT);
+#pragma unroll
+  for (int c = 0; c < RawIdx<IT, N>::C; ++c) {
+    const uint32_t ws[4] = {r.w[c].x, r.w[c].y, r.w[c].z, r.w[c].w};
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const uint32_t word = ws[(e * sizeof(IT)) / 4];
+      const int sh = (e * sizeof(IT) * 8) % 32;
+      int val;
+      if constexpr (sizeof(IT) == 1) val = (int)(int8_t)(word >> sh);
+      else if constexpr (sizeof(IT) == 2) val = (int)(int16_t)(word >> sh);
+      else val = (int)word;
+      dst[c * PER + e] = (double)val;
+    }
+  }
+}
+
 template <int D, int E, typename IT, int FK, typename TOut>
 __global__ void __launch_bounds__(Tile<D, E>::NT)
 k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
@@ -89,10 +122,24 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
 
   int buf = 0;
   if (stage_in) prefetch(blockIdx.x, 0);
+  // whole-block direct loads (full mask, one thread per block): the next
+  // tile's indices and maximum are fetched into registers before this tile's
+  // transform runs, so loads overlap the FMA chain
+  constexpr bool REGPF = (NIN * sizeof(IT)) % 16 == 0 && TL::TB == 1 && NIN <= 16;
+  RawIdx<IT, NIN> raw;
+  double n_next = 0.0;
+  auto reg_prefetch = [&](int64_t tile) {
+    const int64_t bn = tile * BPC + lb;
+    const bool ok = tile < f.ntiles && bn < f.nblocks;
+    load_raw<IT, NIN>(indices + (ok ? bn : 0) * (int64_t)NIN, ok, raw);
+    n_next = ok ? load_kind<FK>(maxima, bn) : 0.0;
+  };
+  if (REGPF && !stage_in) reg_prefetch(blockIdx.x);
   for (int64_t tile = blockIdx.x; tile < f.ntiles; tile += gridDim.x, buf ^= 1) {
     const int64_t b0 = tile * BPC;
     const int64_t b = b0 + lb;
     const bool valid = b < f.nblocks;
+    double n_cur = 0.0;
 
     // ---- first slice (axis 0, axis D-1) at o, as f64 integers
     double v[NIN];
@@ -112,6 +159,10 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
           const int rk = f.full_mask ? pos : rks[pos];
           v[i * E + j] = (valid && rk >= 0) ? (double)st[lb * f.kept + rk] : 0.0;
         }
+    } else if constexpr (REGPF) {
+      unpack_raw<IT, NIN>(raw, v);
+      n_cur = n_next;
+      reg_prefetch(tile + gridDim.x);
     } else {
       if (valid) {
         if constexpr ((NIN * sizeof(IT)) % 16 == 0) {
@@ -155,7 +206,7 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
 
     // ---- scale ((y * N) / r) and store the output slice (axis D-2 rows, D-1 cols)
     if (valid) {
-      const double n = load_kind<FK>(maxima, b);
+      const double n = (REGPF && !stage_in) ? n_cur : load_kind<FK>(maxima, b);
       const bool safe = (n >= 0x1p-900) && (n <= nsafe);
       if (safe) {
 #pragma unroll

@@ -73,19 +73,29 @@ struct MomState {
   double cnt = 0, pa = 0, pb = 0, sa = 0, sb = 0, sab = 0, saa = 0, sbb = 0;
   double Sab = 0, Saa = 0, Sbb = 0;
 
+  // PAIR = false: only the a-terms are accumulated (finish() mirrors them)
+  template <bool PAIR = true>
   __device__ __forceinline__ void add_block(double iab, double iaa, double ibb, double fa0,
                                             double fb0, double na, double nb, bool dc) {
-    Sab = __fma_rn(iab, na * nb, Sab);
     Saa = __fma_rn(iaa, na * na, Saa);
-    Sbb = __fma_rn(ibb, nb * nb, Sbb);
+    if (PAIR) {
+      Sab = __fma_rn(iab, na * nb, Sab);
+      Sbb = __fma_rn(ibb, nb * nb, Sbb);
+    }
     if (dc) {
-      const double dca = fa0 * na, dcb = fb0 * nb;
-      if (cnt == 0.0) { pa = dca; pb = dcb; }
-      const double xa = dca - pa, xb = dcb - pb;
-      sa += xa; sb += xb;
-      sab = __fma_rn(xa, xb, sab);
+      const double dca = fa0 * na;
+      if (cnt == 0.0) pa = dca;
+      const double xa = dca - pa;
+      sa += xa;
       saa = __fma_rn(xa, xa, saa);
-      sbb = __fma_rn(xb, xb, sbb);
+      if (PAIR) {
+        const double dcb = fb0 * nb;
+        if (cnt == 0.0) pb = dcb;
+        const double xb = dcb - pb;
+        sb += xb;
+        sab = __fma_rn(xa, xb, sab);
+        sbb = __fma_rn(xb, xb, sbb);
+      }
     }
     cnt += 1.0;
   }
@@ -261,15 +271,18 @@ __device__ __forceinline__ void part_values(const Part<IT>& p, double fa0, doubl
 }
 
 // ------------------------------------------- aligned blocks, vector loads --
-// K*sizeof(IT) is a multiple of 16.  GS lanes per block, NCH 16-byte chunks
-// per lane per block, U blocks per group per iteration.
-template <typename IT, int GS, int U, bool PAIR>
-__global__ void __launch_bounds__(256, 3)
+// K*sizeof(IT) is a multiple of 16.  GS lanes per block, each loading NCH
+// 16-byte chunks per block (NCH = 0: run-time count), U blocks per group per
+// iteration; every chunk of an iteration is loaded before any is consumed so
+// a thread keeps U*NCH*16 bytes (per operand) in flight.
+template <typename IT, int GS, int NCH, int U, bool PAIR>
+__global__ void __launch_bounds__(256, 2)
 k_moments_vec(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
               const void* __restrict__ a_max, const IT* __restrict__ a_idx,
               const void* __restrict__ b_max, const IT* __restrict__ b_idx,
               double* __restrict__ ws, double* __restrict__ record) {
   constexpr int V = 16 / sizeof(IT);
+  constexpr int NC = NCH > 0 ? NCH : 1;  // chunks held per (u) at once
   const int lane = threadIdx.x & 31;
   const int sub = lane % GS;
   const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1) << (lane - sub));
@@ -277,16 +290,16 @@ k_moments_vec(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int gw = lane / GS;       // group within the warp
-  const int nch = kept / (GS * V);  // chunks per lane per block
+  const int nch = NCH > 0 ? NCH : kept / (GS * V);  // chunks per lane per block
   const bool dc = keeps_first != 0;
   MomState st;
+  using F0 = typename std::conditional<sizeof(IT) == 8, long long, int>::type;
   // the warp owns U*GPW consecutive blocks per iteration; block of (u, group)
   // is base + u*GPW + gw, so every load instruction covers a contiguous range
   for (int64_t base = warp * (U * GPW); base < nblocks; base += nwarps * (U * GPW)) {
     const int64_t bb = base + gw;  // block for u is bb + u*GPW
     double na[U], nb[U];
     Part<IT> p[U];
-    using F0 = typename std::conditional<sizeof(IT) == 8, long long, int>::type;
     F0 f0a[U], f0b[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -297,21 +310,25 @@ k_moments_vec(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
         nb[u] = PAIR ? load_kind_rt(b_max, bb + u * GPW, fk_b) : na[u];
       }
     }
-    for (int ch = 0; ch < nch; ++ch) {
-      uint4 wa[U], wb[U];
+    for (int c0 = 0; c0 < nch; c0 += NC) {
+      uint4 wa[U][NC], wb[U][NC];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t off = (bb + u * GPW) * (int64_t)kept + (int64_t)(ch * GS + sub) * V;
         const bool ok = bb + u * GPW < nblocks;
-        wa[u] = ok ? __ldcs(reinterpret_cast<const uint4*>(a_idx + off)) : make_uint4(0, 0, 0, 0);
-        wb[u] = (PAIR && ok) ? __ldcs(reinterpret_cast<const uint4*>(b_idx + off)) : wa[u];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int64_t off = (bb + u * GPW) * (int64_t)kept + (int64_t)((c0 + c) * GS + sub) * V;
+          wa[u][c] = ok ? __ldcs(reinterpret_cast<const uint4*>(a_idx + off)) : make_uint4(0, 0, 0, 0);
+          wb[u][c] = (PAIR && ok) ? __ldcs(reinterpret_cast<const uint4*>(b_idx + off)) : wa[u][c];
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        part_vec<IT, PAIR>(p[u], wa[u], wb[u]);
-        if (ch == 0 && sub == 0) {
-          f0a[u] = (F0)first_elem<IT>(wa[u]);
-          f0b[u] = (F0)first_elem<IT>(wb[u]);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) part_vec<IT, PAIR>(p[u], wa[u][c], wb[u][c]);
+        if (c0 == 0 && sub == 0) {
+          f0a[u] = (F0)first_elem<IT>(wa[u][0]);
+          f0b[u] = (F0)first_elem<IT>(wb[u][0]);
         }
       }
     }
@@ -321,7 +338,7 @@ k_moments_vec(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
       if (sub == 0 && bb + u * GPW < nblocks) {
         double iab, iaa, ibb;
         part_values<IT>(p[u], (double)f0a[u], (double)f0b[u], dc, iab, iaa, ibb);
-        st.add_block(iab, iaa, ibb, (double)f0a[u], (double)f0b[u], na[u], nb[u], dc);
+        st.add_block<PAIR>(iab, iaa, ibb, (double)f0a[u], (double)f0b[u], na[u], nb[u], dc);
       }
     }
   }
@@ -403,7 +420,7 @@ k_moments_staged(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
       }
       const double na = load_kind_rt(a_max, b, fk_a);
       const double nb = PAIR ? load_kind_rt(b_max, b, fk_b) : na;
-      st.add_block(iab, iaa, ibb, fa0, fb0, na, nb, d);
+      st.add_block<PAIR>(iab, iaa, ibb, fa0, fb0, na, nb, d);
     }
     __syncthreads();
   }
@@ -412,7 +429,7 @@ k_moments_staged(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
 
 // ------------------------------------------------- first coefficients only --
 template <typename IT, int U, bool PAIR>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, 2)
 k_moments_dc(int64_t nblocks, int kept, int fk_a, int fk_b, const void* __restrict__ a_max,
              const IT* __restrict__ a_idx, const void* __restrict__ b_max,
              const IT* __restrict__ b_idx, double* __restrict__ ws,
@@ -433,7 +450,7 @@ k_moments_dc(int64_t nblocks, int kept, int fk_a, int fk_b, const void* __restri
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (bb + u * nth < nblocks) st.add_block(0, 0, 0, fa[u], fb[u], na[u], nb[u], true);
+      if (bb + u * nth < nblocks) st.add_block<PAIR>(0, 0, 0, fa[u], fb[u], na[u], nb[u], true);
   }
   finish(st.record(true), ws, PAIR, record);
 }
@@ -463,7 +480,7 @@ static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const v
   const int64_t B = ga.nblocks;
   const int kept = ga.kept;
   if (dc_only && kept > 0) {
-    constexpr int U = 4;
+    constexpr int U = 8;
     auto kern = k_moments_dc<IT, U, PAIR>;
     const int grid = persistent_grid(kern, 256, 0, (B + 256 * U - 1) / (256 * U));
     kern<<<grid, 256, 0, s>>>(B, kept, ga.float_kind, gb.float_kind, a_max, (const IT*)a_idx,
@@ -474,23 +491,33 @@ static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const v
                        !(((uintptr_t)a_idx | (PAIR ? (uintptr_t)b_idx : 0)) & 15);
   if (aligned) {
     const int vecs = kept / V;  // 16-byte chunks per block
-    int GS = 1;  // blocks of <= 64 bytes: one lane owns whole blocks
-    if (vecs > 4) {
-      while (GS < 32 && GS < vecs) GS <<= 1;
-      if (vecs % GS) GS = 1;  // chunks must split evenly over the group
-    }
-    constexpr int U = PAIR ? 2 : 4;
-    const int64_t work = (B * GS + 256 * U - 1) / (256 * U);  // CTAs for one sweep
-#define BZ_GS(G)                                                                          \
-  case G: {                                                                               \
-    auto kern = k_moments_vec<IT, G, U, PAIR>;                                            \
+    // lanes of a group read consecutive chunks: GS = largest power of two
+    // <= 32 dividing the chunk count, each lane NCH = vecs / GS chunks
+    int GS = 1;
+    while (GS < 32 && vecs % (2 * GS) == 0) GS <<= 1;
+    const int nch = vecs / GS;
+    const int NCHs = nch == 1 ? 1 : nch == 2 ? 2 : nch == 4 ? 4 : 0;
+#define BZ_MV(G, N)                                                                       \
+  {                                                                                       \
+    constexpr int U = N == 0 ? 1 : std::max(1, (PAIR ? 2 : 8) / (N * (sizeof(IT) >= 4 ? 2 : 1))); \
+    auto kern = k_moments_vec<IT, G, N, U, PAIR>;                                         \
+    const int64_t work = (B * G + 256 * U - 1) / (256 * U);                               \
     const int grid = persistent_grid(kern, 256, 0, work);                                 \
     kern<<<grid, 256, 0, s>>>(B, kept, ga.keeps_first, ga.float_kind, gb.float_kind, a_max, \
                               (const IT*)a_idx, b_max, (const IT*)b_idx, ws, record);       \
-    break;                                                                                \
   }
+#define BZ_GS(G)                                                   \
+  case G:                                                          \
+    switch (NCHs) {                                                \
+      case 1: BZ_MV(G, 1) break;                                   \
+      case 2: BZ_MV(G, 2) break;                                   \
+      case 4: BZ_MV(G, 4) break;                                   \
+      default: BZ_MV(G, 0) break;                                  \
+    }                                                              \
+    break;
     switch (GS) { BZ_GS(1) BZ_GS(2) BZ_GS(4) BZ_GS(8) BZ_GS(16) BZ_GS(32) }
 #undef BZ_GS
+#undef BZ_MV
     return check_launch("moments_vec");
   }
   // unaligned (or empty) blocks: stage tiles of 256 blocks in shared memory

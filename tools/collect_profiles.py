@@ -28,7 +28,8 @@ from ncu_summary import summarise  # noqa: E402
 OP_KERNELS = {  # bench op -> kernel name prefix
     "compress": ("k_fast_compress", "k_half3_compress", "k_line3_compress", "k_exact_compress"),
     "decompress": ("k_fast_decompress", "k_half3_decompress", "k_line3_decompress", "k_exact_decompress"),
-    "l2_norm": ("k_moments_vec", "k_moments_staged"),
+    "l2_norm": ("k_moments_vec", "k_moments_staged"),  # PAIR = 0 instantiation
+    "dot": ("k_moments_vec", "k_moments_staged"),      # PAIR = 1
     "add": ("k_add",),
 }
 
@@ -109,11 +110,13 @@ def main():
             lines.append(f"{name[:58]:58s} {len(t):8d} {med / 1e3:10.1f} "
                          f"{(statistics.median(dram) / 1e6 if dram else 0):9.1f} {share:6.3f}")
             for op, prefixes in OP_KERNELS.items():
+                if op in ("l2_norm", "dot") and not name.endswith(", 0>" if op == "l2_norm" else ", 1>"):
+                    continue
                 if any(name.split("<")[0].endswith(p) or name.startswith("void " + p) or name.startswith(p)
                        for p in prefixes) and dram:
                     key = f"{w}:{op}"
                     if "to_kind" not in key:
-                        traffic.setdefault(key, statistics.median(dram))
+                        traffic[key] = statistics.median(dram)
         with open(os.path.join(prof, f"{tag}_launches_{w}.txt"), "w") as fh:
             fh.write("\n".join(lines) + "\n")
 

@@ -1,0 +1,62 @@
+"""Host-side latency of the scalar reductions (what a caller of l2_norm/mean waits).
+
+    python tools/latency_probe.py [c2]
+
+Prints wall-clock microseconds per call for: the fused kernel alone (device
+time, CUDA events), the launch call alone (host time), the record readback,
+the whole public call, and a cProfile of the public call.
+"""
+
+import cProfile
+import os
+import pstats
+import sys
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+import paper_2406_11209_b200 as bz  # noqa: E402
+from paper_2406_11209_b200 import ops  # noqa: E402
+from quick_bench import CONFIGS, fill, timeit  # noqa: E402
+
+
+def wall(fn, reps=200):
+    for _ in range(10):
+        fn()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) / reps * 1e6
+
+
+def main(name):
+    shape, block, fk, ik, _ = CONFIGS[name]
+    s = bz.CodecSettings(block, bz.FloatKind(fk), bz.IndexKind(ik))
+    for shp in [(64,) * len(shape), shape]:
+        x = fill(shp, bz.FloatKind(fk), 1)
+        ca = bz.compress(x, s)
+        rec = ops.moments_record(ca)
+        print(f"== {name} {shp}")
+        print(f"  kernel l2 (events)      {timeit(lambda: ops.moments_record(ca), 50) * 1e3:8.1f} us")
+        print(f"  kernel dc (events)      {timeit(lambda: ops.moments_record(ca, dc_only=True), 50) * 1e3:8.1f} us")
+        print(f"  launch only (host)      {wall(lambda: ops.moments_record(ca)):8.1f} us")
+        print(f"  record_to_host          {wall(lambda: ops.record_to_host(rec)):8.1f} us")
+        print(f"  l2_norm (public)        {wall(lambda: bz.l2_norm(ca)):8.1f} us")
+        print(f"  mean (public)           {wall(lambda: bz.mean(ca)):8.1f} us")
+        print(f"  dot (public)            {wall(lambda: bz.dot(ca, ca)):8.1f} us")
+    pr = cProfile.Profile()
+    pr.enable()
+    for _ in range(200):
+        bz.l2_norm(ca)
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(14)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "c2")
