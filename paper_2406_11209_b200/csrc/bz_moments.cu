@@ -9,11 +9,11 @@
 //   DC_x  = Fx0*Nx, accumulated as pivot-shifted sums per thread and turned
 //           into (n, mean, centred co-moment) records merged with Chan's
 //           formulas (warp tree -> CTA -> one deterministic final tree).
-// Streaming layout: GS lanes share a block, each loading 16-byte vectors;
-// every group works on U consecutive blocks per iteration so U*16 bytes per
-// lane and operand are in flight.  Blocks whose kept indices are not a whole
-// number of 16-byte vectors (e.g. C5's 66-byte blocks) are staged through
-// shared memory in coalesced tiles and reduced one block per thread.
+// Streaming layout: the index arrays are read as a flat stream of 32-byte
+// chunks (256-bit LDGs), U per operand in flight per thread, each scaled by
+// its block's Na*Nb on the spot (see k_moments_stream).  Blocks smaller than
+// one 16-byte vector are staged through shared memory and reduced one block
+// per thread.
 #include "bz_common.cuh"
 #include "bz_kernels.cuh"
 
@@ -82,6 +82,36 @@ struct MomState {
       Sab = __fma_rn(iab, na * nb, Sab);
       Sbb = __fma_rn(ibb, nb * nb, Sbb);
     }
+    if (dc) {
+      const double dca = fa0 * na;
+      if (cnt == 0.0) pa = dca;
+      const double xa = dca - pa;
+      sa += xa;
+      saa = __fma_rn(xa, xa, saa);
+      if (PAIR) {
+        const double dcb = fb0 * nb;
+        if (cnt == 0.0) pb = dcb;
+        const double xb = dcb - pb;
+        sb += xb;
+        sab = __fma_rn(xa, xb, sab);
+        sbb = __fma_rn(xb, xb, sbb);
+      }
+    }
+    cnt += 1.0;
+  }
+
+  // AC part of one block segment (linear: segments may be added separately)
+  template <bool PAIR = true>
+  __device__ __forceinline__ void add_ac(double iab, double iaa, double ibb, double na, double nb) {
+    Saa = __fma_rn(iaa, na * na, Saa);
+    if (PAIR) {
+      Sab = __fma_rn(iab, na * nb, Sab);
+      Sbb = __fma_rn(ibb, nb * nb, Sbb);
+    }
+  }
+  // once per block: its DC value (when the mask keeps it) and the block count
+  template <bool PAIR = true>
+  __device__ __forceinline__ void add_dc(double fa0, double fb0, double na, double nb, bool dc) {
     if (dc) {
       const double dca = fa0 * na;
       if (cnt == 0.0) pa = dca;
@@ -179,167 +209,276 @@ __device__ __forceinline__ void finish(Rec r, double* __restrict__ ws, int pair,
   }
 }
 
-// ------------------------------------------------ integer block partials --
-template <typename IT>
-struct Part {  // exact per-lane partial sums of one block (f64 for 32/64-bit kinds)
-  using T = typename std::conditional<(sizeof(IT) <= 2), long long, double>::type;
-  T ab = 0, aa = 0, bb = 0;
+// --------------------------------------------------- streaming chunks --
+// The index arrays are read as one contiguous stream of CW-byte chunks
+// (CW = 32: one 256-bit LDG per chunk; 16 when the base is only 16-byte
+// aligned), grid-strided so every load instruction of a warp covers a
+// contiguous range, U chunks per operand in flight per thread together with
+// the maxima they need (their addresses depend only on the position, so no
+// load waits on another).  A chunk holds indices of at most two blocks
+// (K >= V): block b for its first element and -- when the next block starts
+// inside the chunk at p = K - off < V -- block b + 1 for the rest.  The AC
+// sums are linear, so each segment's exact integer sum is scaled by its
+// block's Na*Nb and accumulated per thread in f64: no per-block cross-lane
+// reduction.  The chunk holding a block's first element also feeds that
+// block's DC value into the pivot-shifted moments (MomState).
+template <int NW>
+struct Chunk {
+  unsigned w[NW];
 };
 
-template <typename IT, bool PAIR>
-__device__ __forceinline__ void part_vec(Part<IT>& p, const uint4& wa, const uint4& wb) {
+template <int NW>
+__device__ __forceinline__ Chunk<NW> ld_chunk(const void* p) {
+  Chunk<NW> c;
+  if constexpr (NW == 8) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3]), "=r"(c.w[4]),
+                   "=r"(c.w[5]), "=r"(c.w[6]), "=r"(c.w[7])
+                 : "l"(p));
+  } else {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p));
+    c.w[0] = v.x; c.w[1] = v.y; c.w[2] = v.z; c.w[3] = v.w;
+  }
+  return c;
+}
+
+template <typename IT>
+struct SegSums {
+  using T = typename std::conditional<(sizeof(IT) <= 2), long long, double>::type;
+  T ab[2] = {0, 0}, aa[2] = {0, 0}, bb[2] = {0, 0};
+};
+
+// byte mask of word w for the elements [0, p_bytes) of a chunk
+__device__ __forceinline__ unsigned word_mask(int p_bytes, int w) {
+  const int m = p_bytes - 4 * w;
+  return m >= 4 ? 0xffffffffu : (m <= 0 ? 0u : ((1u << (8 * m)) - 1u));
+}
+
+// exact sums of the chunk's elements [0, p) (segment 0) and [p, V) (segment 1)
+template <typename IT, bool PAIR, int NW>
+__device__ __forceinline__ void seg_sums(SegSums<IT>& s, const Chunk<NW>& a, const Chunk<NW>& b,
+                                         int p) {
+  constexpr int V = NW * 4 / (int)sizeof(IT);
   if constexpr (sizeof(IT) == 1) {
-    int saa = 0, sab = 0, sbb = 0;
-    saa = __dp4a((int)wa.x, (int)wa.x, saa); saa = __dp4a((int)wa.y, (int)wa.y, saa);
-    saa = __dp4a((int)wa.z, (int)wa.z, saa); saa = __dp4a((int)wa.w, (int)wa.w, saa);
-    if (PAIR) {
-      sab = __dp4a((int)wa.x, (int)wb.x, sab); sab = __dp4a((int)wa.y, (int)wb.y, sab);
-      sab = __dp4a((int)wa.z, (int)wb.z, sab); sab = __dp4a((int)wa.w, (int)wb.w, sab);
-      sbb = __dp4a((int)wb.x, (int)wb.x, sbb); sbb = __dp4a((int)wb.y, (int)wb.y, sbb);
-      sbb = __dp4a((int)wb.z, (int)wb.z, sbb); sbb = __dp4a((int)wb.w, (int)wb.w, sbb);
-    }
-    p.aa += saa; p.ab += sab; p.bb += sbb;
-  } else if constexpr (sizeof(IT) == 2) {
-    const uint32_t xa[4] = {wa.x, wa.y, wa.z, wa.w}, xb[4] = {wb.x, wb.y, wb.z, wb.w};
+    int a0 = 0, ab0 = 0, b0 = 0, a1 = 0, ab1 = 0, b1 = 0;
+    if (p >= V) {
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const int a0 = (int)(int16_t)(xa[w] & 0xffff), a1 = (int)(int16_t)(xa[w] >> 16);
-      p.aa += (long long)(a0 * a0 + a1 * a1);  // < 2^31 per pair
-      if (PAIR) {
-        const int b0 = (int)(int16_t)(xb[w] & 0xffff), b1 = (int)(int16_t)(xb[w] >> 16);
-        p.ab += (long long)(a0 * b0) + (long long)(a1 * b1);
-        p.bb += (long long)(b0 * b0 + b1 * b1);
+      for (int w = 0; w < NW; ++w) {
+        a0 = __dp4a((int)a.w[w], (int)a.w[w], a0);
+        if (PAIR) { ab0 = __dp4a((int)a.w[w], (int)b.w[w], ab0); b0 = __dp4a((int)b.w[w], (int)b.w[w], b0); }
+      }
+    } else {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const unsigned m = word_mask(p, w);
+        const int la = (int)(a.w[w] & m), ha = (int)(a.w[w] & ~m);
+        a0 = __dp4a(la, la, a0);
+        a1 = __dp4a(ha, ha, a1);
+        if (PAIR) {
+          const int lb = (int)(b.w[w] & m), hb = (int)(b.w[w] & ~m);
+          ab0 = __dp4a(la, lb, ab0); b0 = __dp4a(lb, lb, b0);
+          ab1 = __dp4a(ha, hb, ab1); b1 = __dp4a(hb, hb, b1);
+        }
       }
     }
-  } else if constexpr (sizeof(IT) == 4) {
-    const int32_t xa[4] = {(int32_t)wa.x, (int32_t)wa.y, (int32_t)wa.z, (int32_t)wa.w};
-    const int32_t xb[4] = {(int32_t)wb.x, (int32_t)wb.y, (int32_t)wb.z, (int32_t)wb.w};
+    s.aa[0] = a0; s.ab[0] = ab0; s.bb[0] = b0;
+    s.aa[1] = a1; s.ab[1] = ab1; s.bb[1] = b1;
+  } else if constexpr (sizeof(IT) == 2) {
+    // pairs of int16 products stay below 2^31 in int32
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const double da = (double)xa[w], db = (double)xb[w];
-      p.aa = __fma_rn(da, da, p.aa);
-      if (PAIR) { p.ab = __fma_rn(da, db, p.ab); p.bb = __fma_rn(db, db, p.bb); }
+    for (int w = 0; w < NW; ++w) {
+      const int x0 = (int)(int16_t)(a.w[w] & 0xffff), x1 = (int)(int16_t)(a.w[w] >> 16);
+      const int y0 = (int)(int16_t)(b.w[w] & 0xffff), y1 = (int)(int16_t)(b.w[w] >> 16);
+      const bool h0 = 2 * w >= p, h1 = 2 * w + 1 >= p;
+      const long long xx0 = x0 * x0, xx1 = x1 * x1;
+      s.aa[0] += (h0 ? 0 : xx0) + (h1 ? 0 : xx1);
+      s.aa[1] += (h0 ? xx0 : 0) + (h1 ? xx1 : 0);
+      if (PAIR) {
+        const long long xy0 = (long long)x0 * y0, xy1 = (long long)x1 * y1;
+        const long long yy0 = y0 * y0, yy1 = y1 * y1;
+        s.ab[0] += (h0 ? 0 : xy0) + (h1 ? 0 : xy1);
+        s.ab[1] += (h0 ? xy0 : 0) + (h1 ? xy1 : 0);
+        s.bb[0] += (h0 ? 0 : yy0) + (h1 ? 0 : yy1);
+        s.bb[1] += (h0 ? yy0 : 0) + (h1 ? yy1 : 0);
+      }
     }
   } else {
-    const long long a0 = (long long)(((unsigned long long)wa.y << 32) | wa.x);
-    const long long a1 = (long long)(((unsigned long long)wa.w << 32) | wa.z);
-    const long long b0 = (long long)(((unsigned long long)wb.y << 32) | wb.x);
-    const long long b1 = (long long)(((unsigned long long)wb.w << 32) | wb.z);
-    p.aa = __fma_rn((double)a0, (double)a0, p.aa);
-    p.aa = __fma_rn((double)a1, (double)a1, p.aa);
-    if (PAIR) {
-      p.ab = __fma_rn((double)a0, (double)b0, p.ab);
-      p.ab = __fma_rn((double)a1, (double)b1, p.ab);
-      p.bb = __fma_rn((double)b0, (double)b0, p.bb);
-      p.bb = __fma_rn((double)b1, (double)b1, p.bb);
+    constexpr int WPE = sizeof(IT) / 4;  // words per element
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      double da, db;
+      if constexpr (WPE == 1) {
+        da = (double)(int32_t)a.w[e];
+        db = (double)(int32_t)b.w[e];
+      } else {
+        da = (double)(long long)(((unsigned long long)a.w[2 * e + 1] << 32) | a.w[2 * e]);
+        db = (double)(long long)(((unsigned long long)b.w[2 * e + 1] << 32) | b.w[2 * e]);
+      }
+      const bool hi = e >= p;
+      const double d0 = hi ? 0.0 : da, d1 = hi ? da : 0.0;
+      s.aa[0] = __fma_rn(d0, d0, s.aa[0]); s.aa[1] = __fma_rn(d1, d1, s.aa[1]);
+      if (PAIR) {
+        const double e0 = hi ? 0.0 : db, e1 = hi ? db : 0.0;
+        s.ab[0] = __fma_rn(d0, e0, s.ab[0]); s.ab[1] = __fma_rn(d1, e1, s.ab[1]);
+        s.bb[0] = __fma_rn(e0, e0, s.bb[0]); s.bb[1] = __fma_rn(e1, e1, s.bb[1]);
+      }
     }
   }
+}
+
+template <int NW>
+__device__ __forceinline__ unsigned chunk_word(const Chunk<NW>& c, int i) {
+  unsigned r = c.w[0];
+#pragma unroll
+  for (int k = 1; k < NW; ++k) r = i == k ? c.w[k] : r;
+  return r;
+}
+
+template <typename IT, int NW>
+__device__ __forceinline__ long long chunk_elem(const Chunk<NW>& c, int e) {
+  if constexpr (sizeof(IT) == 1) {
+    return (long long)(int8_t)((chunk_word(c, e >> 2) >> (8 * (e & 3))) & 0xff);
+  } else if constexpr (sizeof(IT) == 2) {
+    return (long long)(int16_t)((chunk_word(c, e >> 1) >> (16 * (e & 1))) & 0xffff);
+  } else if constexpr (sizeof(IT) == 4) {
+    return (long long)(int32_t)chunk_word(c, e);
+  } else {
+    return (long long)(((unsigned long long)chunk_word(c, 2 * e + 1) << 32) | chunk_word(c, 2 * e));
+  }
+}
+
+template <int FK>
+__device__ __forceinline__ double ld_max(const void* p, int64_t i, int fk) {
+  if constexpr (FK >= 0) return load_kind<FK>(p, i);
+  else return load_kind_rt(p, i, fk);
 }
 
 template <typename IT>
-__device__ __forceinline__ long long first_elem(const uint4& w) {
-  if constexpr (sizeof(IT) == 1) return (long long)(int8_t)(w.x & 0xff);
-  else if constexpr (sizeof(IT) == 2) return (long long)(int16_t)(w.x & 0xffff);
-  else if constexpr (sizeof(IT) == 4) return (long long)(int32_t)w.x;
-  else return (long long)(((unsigned long long)w.y << 32) | w.x);
+__device__ __forceinline__ typename SegSums<IT>::T sprod(long long x, long long y) {
+  if constexpr (sizeof(IT) <= 2) return x * y;
+  else return (double)x * (double)y;
 }
 
-template <typename IT, bool PAIR>
-__device__ __forceinline__ void part_reduce(Part<IT>& p, unsigned mask, int width) {
-  for (int o = width / 2; o > 0; o >>= 1) {
-    p.aa += __shfl_xor_sync(mask, p.aa, o, width);
-    if (PAIR) {
-      p.ab += __shfl_xor_sync(mask, p.ab, o, width);
-      p.bb += __shfl_xor_sync(mask, p.bb, o, width);
-    }
+// position (block, offset) of a chunk's first element, advanced incrementally
+// (no per-chunk division): a step of `nth` chunks is qs blocks + rs elements
+struct ChunkPos {
+  int64_t b;
+  int off;
+  __device__ __forceinline__ void advance(int64_t qs, int rs, int kept) {
+    b += qs;
+    off += rs;
+    if (off >= kept) { off -= kept; ++b; }
   }
-}
+};
 
-template <typename IT>
-__device__ __forceinline__ void part_values(const Part<IT>& p, double fa0, double fb0, bool dc,
-                                            double& iab, double& iaa, double& ibb) {
-  if constexpr (sizeof(IT) <= 2) {
-    const long long a0 = (long long)fa0, b0 = (long long)fb0;
-    iab = (double)(p.ab - (dc ? a0 * b0 : 0));
-    iaa = (double)(p.aa - (dc ? a0 * a0 : 0));
-    ibb = (double)(p.bb - (dc ? b0 * b0 : 0));
-  } else {
-    iab = p.ab - (dc ? fa0 * fb0 : 0.0);
-    iaa = p.aa - (dc ? fa0 * fa0 : 0.0);
-    ibb = p.bb - (dc ? fb0 * fb0 : 0.0);
-  }
-}
-
-// ------------------------------------------- aligned blocks, vector loads --
-// K*sizeof(IT) is a multiple of 16.  GS lanes per block, each loading NCH
-// 16-byte chunks per block (NCH = 0: run-time count), U blocks per group per
-// iteration; every chunk of an iteration is loaded before any is consumed so
-// a thread keeps U*NCH*16 bytes (per operand) in flight.
-template <typename IT, int GS, int NCH, int U, bool PAIR>
+// FK >= 0: both operands' maxima are of float kind FK (compile time);
+// SPAN = false: K is a multiple of V, no chunk crosses a block boundary
+template <typename IT, int NW, int U, bool PAIR, int FK, bool SPAN>
 __global__ void __launch_bounds__(256, 2)
-k_moments_vec(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
-              const void* __restrict__ a_max, const IT* __restrict__ a_idx,
-              const void* __restrict__ b_max, const IT* __restrict__ b_idx,
-              double* __restrict__ ws, double* __restrict__ record) {
-  constexpr int V = 16 / sizeof(IT);
-  constexpr int NC = NCH > 0 ? NCH : 1;  // chunks held per (u) at once
-  const int lane = threadIdx.x & 31;
-  const int sub = lane % GS;
-  const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1) << (lane - sub));
-  constexpr int GPW = 32 / GS;  // groups per warp
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int gw = lane / GS;       // group within the warp
-  const int nch = NCH > 0 ? NCH : kept / (GS * V);  // chunks per lane per block
+k_moments_stream(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
+                 const void* __restrict__ a_max, const IT* __restrict__ a_idx,
+                 const void* __restrict__ b_max, const IT* __restrict__ b_idx,
+                 double* __restrict__ ws, double* __restrict__ record) {
+  constexpr int CW = NW * 4;
+  constexpr int V = CW / (int)sizeof(IT);
+  const int64_t total = nblocks * (int64_t)kept;
+  const int64_t nchunks = total / V;  // whole chunks (tail below)
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool dc = keeps_first != 0;
   MomState st;
-  using F0 = typename std::conditional<sizeof(IT) == 8, long long, int>::type;
-  // the warp owns U*GPW consecutive blocks per iteration; block of (u, group)
-  // is base + u*GPW + gw, so every load instruction covers a contiguous range
-  for (int64_t base = warp * (U * GPW); base < nblocks; base += nwarps * (U * GPW)) {
-    const int64_t bb = base + gw;  // block for u is bb + u*GPW
-    double na[U], nb[U];
-    Part<IT> p[U];
-    F0 f0a[U], f0b[U];
+  const unsigned char* ca = reinterpret_cast<const unsigned char*>(a_idx);
+  const unsigned char* cb = reinterpret_cast<const unsigned char*>(b_idx);
+  const int64_t qs = (nth * V) / kept;
+  const int rs = (int)(nth * V - qs * kept);
+
+  // f32 maxima stay 32-bit until used
+  using MT = typename std::conditional<FK == BZ_F32, float, double>::type;
+  struct Nm {
+    MT a0, b0, a1, b1;
+  };
+  auto ldn = [&](const void* p, int64_t i, int fk) -> MT {
+    if constexpr (FK == BZ_F32) return __ldg(reinterpret_cast<const float*>(p) + i);
+    else return ld_max<FK>(p, i, fk);
+  };
+  auto load_n = [&](const ChunkPos& cp) {
+    Nm n;
+    n.a0 = ldn(a_max, cp.b, fk_a);
+    n.b0 = PAIR ? ldn(b_max, cp.b, fk_b) : n.a0;
+    n.a1 = n.b1 = 0;
+    if (SPAN && kept - cp.off < V) {
+      n.a1 = ldn(a_max, cp.b + 1, fk_a);
+      n.b1 = PAIR ? ldn(b_max, cp.b + 1, fk_b) : n.a1;
+    }
+    return n;
+  };
+  auto consume = [&](const ChunkPos& cp, const Chunk<NW>& wa, const Chunk<NW>& wb, const Nm& n) {
+    const int p = SPAN ? kept - cp.off : V;  // elements of block cp.b in this chunk = min(p, V)
+    SegSums<IT> s;
+    seg_sums<IT, PAIR, NW>(s, wa, wb, p);
+    if (cp.off == 0) {  // block b starts here: element 0 is its DC
+      const long long x0 = chunk_elem<IT, NW>(wa, 0), y0 = PAIR ? chunk_elem<IT, NW>(wb, 0) : x0;
+      if (dc) {
+        s.aa[0] -= sprod<IT>(x0, x0);
+        if (PAIR) { s.ab[0] -= sprod<IT>(x0, y0); s.bb[0] -= sprod<IT>(y0, y0); }
+      }
+      st.template add_dc<PAIR>((double)x0, (double)y0, (double)n.a0, (double)n.b0, dc);
+    }
+    st.template add_ac<PAIR>((double)s.ab[0], (double)s.aa[0], (double)s.bb[0], (double)n.a0,
+                             (double)n.b0);
+    if (SPAN && p < V) {  // block b + 1 starts at element p
+      const long long x0 = chunk_elem<IT, NW>(wa, p), y0 = PAIR ? chunk_elem<IT, NW>(wb, p) : x0;
+      if (dc) {
+        s.aa[1] -= sprod<IT>(x0, x0);
+        if (PAIR) { s.ab[1] -= sprod<IT>(x0, y0); s.bb[1] -= sprod<IT>(y0, y0); }
+      }
+      st.template add_dc<PAIR>((double)x0, (double)y0, (double)n.a1, (double)n.b1, dc);
+      st.template add_ac<PAIR>((double)s.ab[1], (double)s.aa[1], (double)s.bb[1], (double)n.a1,
+                               (double)n.b1);
+    }
+  };
+
+  ChunkPos cp;
+  {
+    const int64_t e0 = tid * V;
+    cp.b = e0 / kept;
+    cp.off = (int)(e0 - cp.b * kept);
+  }
+  int64_t c = tid;
+  for (; c + (U - 1) * nth < nchunks; c += U * nth) {
+    Chunk<NW> wa[U], wb[U];
+    ChunkPos ps[U];
+    Nm nm[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      na[u] = nb[u] = 0.0;
-      f0a[u] = f0b[u] = 0;
-      if (sub == 0 && bb + u * GPW < nblocks) {
-        na[u] = load_kind_rt(a_max, bb + u * GPW, fk_a);
-        nb[u] = PAIR ? load_kind_rt(b_max, bb + u * GPW, fk_b) : na[u];
-      }
-    }
-    for (int c0 = 0; c0 < nch; c0 += NC) {
-      uint4 wa[U][NC], wb[U][NC];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool ok = bb + u * GPW < nblocks;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const int64_t off = (bb + u * GPW) * (int64_t)kept + (int64_t)((c0 + c) * GS + sub) * V;
-          wa[u][c] = ok ? __ldcs(reinterpret_cast<const uint4*>(a_idx + off)) : make_uint4(0, 0, 0, 0);
-          wb[u][c] = (PAIR && ok) ? __ldcs(reinterpret_cast<const uint4*>(b_idx + off)) : wa[u][c];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) part_vec<IT, PAIR>(p[u], wa[u][c], wb[u][c]);
-        if (c0 == 0 && sub == 0) {
-          f0a[u] = (F0)first_elem<IT>(wa[u][0]);
-          f0b[u] = (F0)first_elem<IT>(wb[u][0]);
-        }
-      }
+      ps[u] = cp;
+      cp.advance(qs, rs, kept);
+      wa[u] = ld_chunk<NW>(ca + (c + u * nth) * CW);
+      wb[u] = PAIR ? ld_chunk<NW>(cb + (c + u * nth) * CW) : wa[u];
+      nm[u] = load_n(ps[u]);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      part_reduce<IT, PAIR>(p[u], gmask, GS);
-      if (sub == 0 && bb + u * GPW < nblocks) {
-        double iab, iaa, ibb;
-        part_values<IT>(p[u], (double)f0a[u], (double)f0b[u], dc, iab, iaa, ibb);
-        st.add_block<PAIR>(iab, iaa, ibb, (double)f0a[u], (double)f0b[u], na[u], nb[u], dc);
+    for (int u = 0; u < U; ++u) consume(ps[u], wa[u], wb[u], nm[u]);
+  }
+  for (; c < nchunks; c += nth) {
+    const Chunk<NW> wa = ld_chunk<NW>(ca + c * CW);
+    const Chunk<NW> wb = PAIR ? ld_chunk<NW>(cb + c * CW) : wa;
+    consume(cp, wa, wb, load_n(cp));
+    cp.advance(qs, rs, kept);
+  }
+  // trailing partial chunk (nblocks*kept not a multiple of V): one thread, scalar
+  if (tid == 0 && nchunks * V < total) {
+    for (int64_t e = nchunks * V; e < total; ++e) {
+      const int64_t b = e / kept;
+      const int pos = (int)(e - b * kept);
+      const long long x = (long long)a_idx[e], y = PAIR ? (long long)b_idx[e] : x;
+      const double na = ld_max<FK>(a_max, b, fk_a), nb = PAIR ? ld_max<FK>(b_max, b, fk_b) : na;
+      if (pos == 0) {
+        st.template add_dc<PAIR>((double)x, (double)y, na, nb, dc);
+        if (dc) continue;
       }
+      st.template add_ac<PAIR>((double)sprod<IT>(x, y), (double)sprod<IT>(x, x),
+                               (double)sprod<IT>(y, y), na, nb);
     }
   }
   finish(st.record(dc), ws, PAIR, record);
@@ -476,7 +615,6 @@ template <typename IT, bool PAIR>
 static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                         const void* b_max, const void* b_idx, int dc_only, double* ws,
                         double* record, cudaStream_t s) {
-  constexpr int V = 16 / sizeof(IT);
   const int64_t B = ga.nblocks;
   const int kept = ga.kept;
   if (dc_only && kept > 0) {
@@ -487,38 +625,35 @@ static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const v
                               b_max, (const IT*)b_idx, ws, record);
     return check_launch("moments_dc");
   }
-  const bool aligned = kept > 0 && (kept * sizeof(IT)) % 16 == 0 &&
-                       !(((uintptr_t)a_idx | (PAIR ? (uintptr_t)b_idx : 0)) & 15);
-  if (aligned) {
-    const int vecs = kept / V;  // 16-byte chunks per block
-    // lanes of a group read consecutive chunks: GS = largest power of two
-    // <= 32 dividing the chunk count, each lane NCH = vecs / GS chunks
-    int GS = 1;
-    while (GS < 32 && vecs % (2 * GS) == 0) GS <<= 1;
-    const int nch = vecs / GS;
-    const int NCHs = nch == 1 ? 1 : nch == 2 ? 2 : nch == 4 ? 4 : 0;
-#define BZ_MV(G, N)                                                                       \
-  {                                                                                       \
-    constexpr int U = N == 0 ? 1 : std::max(1, (PAIR ? 2 : 8) / (N * (sizeof(IT) >= 4 ? 2 : 1))); \
-    auto kern = k_moments_vec<IT, G, N, U, PAIR>;                                         \
-    const int64_t work = (B * G + 256 * U - 1) / (256 * U);                               \
-    const int grid = persistent_grid(kern, 256, 0, work);                                 \
-    kern<<<grid, 256, 0, s>>>(B, kept, ga.keeps_first, ga.float_kind, gb.float_kind, a_max, \
-                              (const IT*)a_idx, b_max, (const IT*)b_idx, ws, record);       \
+  const uintptr_t base = (uintptr_t)a_idx | (PAIR ? (uintptr_t)b_idx : 0);
+  // 32-byte chunks (256-bit loads) when aligned; 16-byte otherwise and for 32/64-bit kinds
+  const int nw = (sizeof(IT) <= 2 && kept >= 32 / (int)sizeof(IT) && !(base & 31)) ? 8 : 4;
+  if (kept >= 16 / (int)sizeof(IT) && !(base & 15)) {
+    constexpr int U = PAIR ? 4 : 8;
+    const int64_t chunks = B * (int64_t)kept * sizeof(IT) / (4 * nw);
+    const int fk = ga.float_kind == gb.float_kind ? ga.float_kind : -1;
+#define BZ_MS(NWV, FKV, SP)                                                                      \
+  {                                                                                              \
+    constexpr int UU = NWV == 8 ? U / 2 : U;                                                     \
+    auto kern = k_moments_stream<IT, NWV, UU, PAIR, FKV, SP>;                                    \
+    const int grid = persistent_grid(kern, 256, 0, (chunks + 256 * UU - 1) / (256 * UU));       \
+    kern<<<grid, 256, 0, s>>>(B, kept, ga.keeps_first, ga.float_kind, gb.float_kind, a_max,      \
+                              (const IT*)a_idx, b_max, (const IT*)b_idx, ws, record);            \
+    return check_launch("moments_stream");                                                       \
   }
-#define BZ_GS(G)                                                   \
-  case G:                                                          \
-    switch (NCHs) {                                                \
-      case 1: BZ_MV(G, 1) break;                                   \
-      case 2: BZ_MV(G, 2) break;                                   \
-      case 4: BZ_MV(G, 4) break;                                   \
-      default: BZ_MV(G, 0) break;                                  \
-    }                                                              \
-    break;
-    switch (GS) { BZ_GS(1) BZ_GS(2) BZ_GS(4) BZ_GS(8) BZ_GS(16) BZ_GS(32) }
-#undef BZ_GS
-#undef BZ_MV
-    return check_launch("moments_vec");
+#define BZ_NW(FKV, SPV)                                             \
+  if (nw == 8) { BZ_MS(8, FKV, SPV) } else { BZ_MS(4, FKV, SPV) }
+    if constexpr (sizeof(IT) <= 2) {
+      const bool span8 = kept % (32 / (int)sizeof(IT)) != 0, span4 = kept % (16 / (int)sizeof(IT)) != 0;
+      const bool span = nw == 8 ? span8 : span4;
+      if (fk == BZ_F32) { if (span) { BZ_NW(BZ_F32, true) } else { BZ_NW(BZ_F32, false) } }
+      if (fk == BZ_F64) { if (span) { BZ_NW(BZ_F64, true) } else { BZ_NW(BZ_F64, false) } }
+      BZ_NW(-1, true)
+    } else {
+      BZ_MS(4, -1, true)
+    }
+#undef BZ_NW
+#undef BZ_MS
   }
   // unaligned (or empty) blocks: stage tiles of 256 blocks in shared memory
   const size_t tile = (size_t)256 * kept * sizeof(IT);

@@ -273,3 +273,32 @@ def test_partition_invariance_of_random_fill(bz):
     _native.call("bz_fill_random", full.data_ptr(), 2, full.numel(), 0, 9, 0, s)
     _native.call("bz_fill_random", part.data_ptr(), 2, part.numel(), 1 << 19, 9, 0, s)
     assert torch.equal(full[1 << 19:], part)
+
+
+@pytest.mark.parametrize("block,ik,keep", [
+    ((8, 8), "i8", 5),          # 5 kept < 16 per chunk: staged path
+    ((8, 8), "i16", 37),        # odd kept, chunks span two blocks
+    ((4, 4, 4), "i8", 23),      # spanning, int8 masks inside a chunk
+    ((8, 8), "i32", 64),
+    ((8, 8), "i64", 64),
+    ((16, 16), "i16", 256),
+])
+def test_reductions_mask_and_kinds(bz, block, ik, keep):
+    """Streaming reductions over every index kind and chunk/block alignment."""
+    rng = np.random.default_rng(11)
+    shape = tuple(b * g for b, g in zip(block, (7, 5, 3)[:len(block)]))
+    bits = np.zeros(int(np.prod(block)), bool)
+    bits[0] = True
+    bits[1 + rng.permutation(bits.size - 1)[:keep - 1]] = True
+    bits = bits.reshape(block)
+    s = _settings(bz, block, "f32", ik, mask_bits=bits)
+    os_ = o.Settings(block, "f32", ik, "dct", bits)
+    xa = rng.normal(size=shape)
+    xb = 0.3 * xa + rng.normal(size=shape)
+    ra, rb = o.compress(o.round_to_kind(xa, "f32"), os_), o.compress(o.round_to_kind(xb, "f32"), os_)
+    a = bz.CompressedArray(shape, s, ra.maxima, ra.indices)
+    b = bz.CompressedArray(shape, s, rb.maxima, rb.indices)
+    for k, g, w in (("dot", bz.dot(a, b), o.dot(ra, rb)), ("l2", bz.l2_norm(b), o.l2_norm(rb)),
+                    ("cov", bz.covariance(a, b), o.covariance(ra, rb)),
+                    ("var", bz.variance(a), o.variance(ra)), ("mean", bz.mean(b), o.mean(rb))):
+        assert math.isclose(g, w, rel_tol=1e-9, abs_tol=1e-12), (k, g, w)
