@@ -83,7 +83,7 @@ size_t bz_compress_workspace(const bz_layout* L) {
   Geo g = make_geo(L);
   size_t generic = exact_compress_workspace(g, g.nblocks);
   size_t convert = (size_t)dense_count(L) * float_kind_bytes(L->float_kind) + 256;
-  return std::max(generic, convert) + 256;
+  return std::max(std::max(generic, convert), dct8_compress_workspace(g)) + 256;
 }
 
 int bz_compress(const bz_layout* L, const void* x, int x_kind, void* maxima, void* indices,
@@ -100,6 +100,9 @@ int bz_compress(const bz_layout* L, const void* x, int x_kind, void* maxima, voi
     if (int rc = launch_round_to_kind(x, x_kind, ws, L->float_kind, dense_count(L), nullptr, s)) return rc;
     return launch_fast_compress(g, ws, maxima, indices, s);
   }
+  if (!force_generic() && dct8_compress_supported(g, x_kind) && ws &&
+      ws_bytes >= dct8_compress_workspace(g))
+    return launch_dct8_compress(g, x, maxima, indices, ws, ws_bytes, s);
   if (!force_generic() && fast_supported(g, x_kind))
     return launch_fast_compress(g, x, maxima, indices, s);
   return launch_exact_compress(g, x, x_kind, maxima, indices, nullptr, nullptr, g.nblocks, ws,
@@ -118,6 +121,9 @@ int bz_decompress(const bz_layout* L, const void* maxima, const void* indices, v
   if (int rc = need_matrices(L)) return rc;
   Geo g = make_geo(L);
   if (g.nblocks == 0) return BZ_OK;
+  if (!force_generic() && dct8_supported(g) && (out_kind == BZ_F64 || out_kind == BZ_F32) &&
+      g.index_kind != BZ_I64)
+    return launch_dct8_decompress(g, maxima, indices, out, out_kind, S(stream));
   if (!force_generic() && fast_decompress_supported(g, out_kind))
     return launch_fast_decompress(g, maxima, indices, out, out_kind, S(stream));
   return launch_exact_decompress(g, maxima, indices, out, out_kind, ws, ws_bytes, S(stream));

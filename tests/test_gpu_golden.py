@@ -61,6 +61,10 @@ def gemv_case(case):
     return len(case["block"]) == 1 and int(np.prod(case["maxima"].shape)) == 1
 
 
+# stated tolerance of the default (non-bit-exact) decompress kernels
+DECOMPRESS_RTOL = 1e-13
+
+
 def assert_same(got, ref, case):
     if gemv_case(case):
         span = np.max(np.abs(ref[np.isfinite(ref)])) if np.isfinite(ref).any() else 0.0
@@ -98,10 +102,21 @@ def test_transform_building_blocks_bit_exact(bz, case):
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
-def test_decompress_matches_reference(bz, case):
+def test_decompress_matches_reference(bz, case, monkeypatch):
+    """Exact kernels (BZC_B200_EXACT=1): bit-identical.  Default kernels (the
+    factored 8-point DCT for 8x8x8 blocks): within DECOMPRESS_RTOL of the
+    largest reference magnitude."""
+    monkeypatch.setenv("BZC_B200_EXACT", "1")
     out = bz.decompress(ref_compressed(bz, case))
     assert out.kind is bz.FloatKind.F64
     assert_same(out.numpy(), case["decompressed"], case)
+    monkeypatch.delenv("BZC_B200_EXACT")
+    got = bz.decompress(ref_compressed(bz, case)).numpy()
+    ref = case["decompressed"]
+    fin = np.isfinite(ref)
+    span = np.max(np.abs(ref[fin])) if fin.any() else 0.0
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    assert np.all(np.abs(got[fin] - ref[fin]) <= DECOMPRESS_RTOL * span)
 
 
 @pytest.mark.parametrize("case", OPS, ids=[c["name"] for c in OPS])

@@ -125,10 +125,17 @@ def test_fast_and_generic_agree(bz, monkeypatch, shape, block, fk, ik):
     generic = bz.compress(a, s)
     gen_dec = bz.decompress(fast).values
     monkeypatch.delenv("BZC_B200_FORCE_GENERIC")
-    # both evaluate the reference's FMA chain: identical bits
+    # compress: maxima and indices identical bits (the factored 8^3 kernel
+    # proves or recomputes every block)
     assert torch.equal(fast.maxima, generic.maxima)
     assert torch.equal(fast.indices, generic.indices)
-    assert torch.equal(fast_dec, gen_dec)
+    span = float(gen_dec.abs().max())
+    assert float((fast_dec - gen_dec).abs().max()) <= 1e-13 * span
+    # the exact fused kernels evaluate the reference's FMA chain: identical bits
+    monkeypatch.setenv("BZC_B200_EXACT", "1")
+    assert torch.equal(bz.decompress(fast).values, gen_dec)
+    exact = bz.compress(a, s)
+    assert torch.equal(exact.indices, generic.indices) and torch.equal(exact.maxima, generic.maxima)
 
 
 # ------------------------------------------------------------- building blocks --
@@ -302,3 +309,33 @@ def test_reductions_mask_and_kinds(bz, block, ik, keep):
                     ("cov", bz.covariance(a, b), o.covariance(ra, rb)),
                     ("var", bz.variance(a), o.variance(ra)), ("mean", bz.mean(b), o.mean(rb))):
         assert math.isclose(g, w, rel_tol=1e-9, abs_tol=1e-12), (k, g, w)
+
+
+def test_dct8_flagged_blocks(bz, monkeypatch):
+    """Factored 8^3 compress on blocks that must take the exact fix-up: zero,
+    constant (exact ties), tiny/subnormal, NaN, inf, integer-valued data, and
+    maxima next to an f32 rounding boundary; bit-identical to the exact path."""
+    rng = np.random.default_rng(21)
+    x = rng.normal(size=(32, 32, 48)).astype(np.float32).astype(np.float64)
+    x[0:8, 0:8, 0:8] = 0.0
+    x[0:8, 0:8, 8:16] = 5.0
+    x[0:8, 8:16, 0:8] = rng.normal(size=(8, 8, 8)) * 1e-300
+    x[8:16, 0:8, 0:8] = np.round(rng.normal(size=(8, 8, 8)) * 4)
+    x[8:16, 8:16, 8:16] = rng.normal(size=(8, 8, 8)) * 1e-42  # f32 subnormals
+    x[16:24, 0:8, 0:8] = np.nan
+    x[16:24, 8:16, 16:24][3, 3, 3] = np.inf
+    x[24:32, 24:32, 40:48] = rng.integers(-3, 4, size=(8, 8, 8)) * 0.5
+    s = _settings(bz, (8, 8, 8), "f32", "i8")
+    a = bz.DenseArray.of(x, bz.FloatKind.F32)
+    fast = bz.compress(a, s)
+    monkeypatch.setenv("BZC_B200_EXACT", "1")
+    exact = bz.compress(a, s)
+    monkeypatch.setenv("BZC_B200_FORCE_GENERIC", "1")
+    generic = bz.compress(a, s)
+    for ref in (exact, generic):
+        assert torch.equal(fast.maxima.view(torch.int32), ref.maxima.view(torch.int32))
+        assert torch.equal(fast.indices, ref.indices)
+    os_ = o.Settings((8, 8, 8), "f32", "i8", "dct")
+    want = o.compress(o.round_to_kind(x, "f32"), os_)
+    assert np.array_equal(fast.maxima_f64().cpu().numpy(), want.maxima, equal_nan=True)
+    assert np.array_equal(fast.indices.cpu().numpy(), want.indices)
