@@ -10,10 +10,10 @@ flt = sys.argv[1] if len(sys.argv) > 1 else ""
 cur = None
 rows = {}
 for line in sys.stdin:
-    m = re.search(r"Compiling entry function '(\w+)'", line)
+    m = re.search(r"Function properties for (\w+)", line)
     if m:
         cur = m.group(1)
-        rows[cur] = {}
+        rows.setdefault(cur, {})
         continue
     if cur is None:
         continue
