@@ -456,7 +456,12 @@ k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
           if (z < zlim) {
             TOut* dst = out + (z0 + z) * s0 + y * s1 + x0;
             if (xfull && f.vec_dense) {
-              store_row_vec<TOut, 4>(dst, v + z * 4);
+              if constexpr (sizeof(TOut) == 8) {
+                if (f.vec32) store_row_vec32<TOut, 4>(dst, v + z * 4);
+                else store_row_vec<TOut, 4>(dst, v + z * 4);
+              } else {
+                store_row_vec<TOut, 4>(dst, v + z * 4);
+              }
             } else {
 #pragma unroll
               for (int j = 0; j < 4; ++j)

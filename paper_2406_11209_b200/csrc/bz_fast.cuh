@@ -71,6 +71,7 @@ struct FastGeo {
   int32_t kept;
   int32_t full_mask;
   int32_t vec_dense;  // 16-byte vector access legal on the dense side
+  int32_t vec32;      // 32-byte (256-bit) access legal on the dense side
   const int32_t* rank;
 };
 
@@ -100,6 +101,9 @@ inline bool make_fast_params(const Geo& g, int bpc, const void* dense, int dense
   bool ok = ((uintptr_t)dense % 16 == 0) && ((E * dense_bytes) % 16 == 0);
   for (int a = 0; a + 1 < g.ndim; ++a) ok = ok && ((g.stride[a] * dense_bytes) % 16 == 0);
   f.vec_dense = ok;
+  bool ok32 = ((uintptr_t)dense % 32 == 0) && ((E * dense_bytes) % 32 == 0);
+  for (int a = 0; a + 1 < g.ndim; ++a) ok32 = ok32 && ((g.stride[a] * dense_bytes) % 32 == 0);
+  f.vec32 = ok32;
   if (!g.matrices_host) return false;
   for (int i = 0; i < E * E; ++i) p.H[i] = g.matrices_host[i];  // every axis uses the same E
   return true;
@@ -312,6 +316,34 @@ __device__ __forceinline__ void store_row_vec(T* __restrict__ dst, const double*
 
 template <typename T>
 __host__ __device__ constexpr bool row_vectorizable(int E) { return (E * (int)sizeof(T)) % 16 == 0; }
+
+// 256-bit (32-byte) stores: one STG.E.256 per 32 bytes of a row
+template <typename T, int E>
+__device__ __forceinline__ void store_row_vec32(T* __restrict__ dst, const double* src) {
+  static_assert((E * sizeof(T)) % 32 == 0, "row must be a whole number of 32-byte chunks");
+#pragma unroll
+  for (int c = 0; c < E * (int)sizeof(T) / 32; ++c) {
+    if constexpr (sizeof(T) == 8) {
+      asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};\n" ::"l"(dst + c * 4), "d"(src[c * 4]),
+                   "d"(src[c * 4 + 1]), "d"(src[c * 4 + 2]), "d"(src[c * 4 + 3])
+                   : "memory");
+    } else {
+      asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"l"(dst + c * 8),
+                   "f"((float)src[c * 8]), "f"((float)src[c * 8 + 1]), "f"((float)src[c * 8 + 2]),
+                   "f"((float)src[c * 8 + 3]), "f"((float)src[c * 8 + 4]), "f"((float)src[c * 8 + 5]),
+                   "f"((float)src[c * 8 + 6]), "f"((float)src[c * 8 + 7])
+                   : "memory");
+    }
+  }
+}
+
+// 256-bit load of 32 bytes (read-only path, no L1 allocation)
+__device__ __forceinline__ void ld_global_256(const void* p, uint4& lo, uint4& hi) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z),
+                 "=r"(hi.w)
+               : "l"(p));
+}
 
 // ------------------------------------------------------------- cp.async --
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {

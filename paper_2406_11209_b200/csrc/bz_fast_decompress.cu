@@ -44,9 +44,21 @@ struct RawIdx {
 };
 
 template <typename IT, int N>
-__device__ __forceinline__ void load_raw(const IT* __restrict__ src, bool ok, RawIdx<IT, N>& r) {
+__device__ __forceinline__ void load_raw(const IT* __restrict__ src, bool ok, bool v32,
+                                         RawIdx<IT, N>& r) {
+  constexpr int C = RawIdx<IT, N>::C;
+  if constexpr (C % 2 == 0) {
+    if (v32) {  // 256-bit loads
 #pragma unroll
-  for (int c = 0; c < RawIdx<IT, N>::C; ++c)
+      for (int c = 0; c < C; c += 2) {
+        if (ok) ld_global_256(reinterpret_cast<const uint4*>(src) + c, r.w[c], r.w[c + 1]);
+        else r.w[c] = r.w[c + 1] = make_uint4(0, 0, 0, 0);
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c)
     r.w[c] = ok ? __ldcs(reinterpret_cast<const uint4*>(src) + c) : make_uint4(0, 0, 0, 0);
 }
 
@@ -126,12 +138,13 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
   // tile's indices and maximum are fetched into registers before this tile's
   // transform runs, so loads overlap the FMA chain
   constexpr bool REGPF = (NIN * sizeof(IT)) % 16 == 0 && TL::TB == 1 && NIN <= 16;
+  const bool idx32 = ((uintptr_t)indices % 32) == 0;
   RawIdx<IT, NIN> raw;
   double n_next = 0.0;
   auto reg_prefetch = [&](int64_t tile) {
     const int64_t bn = tile * BPC + lb;
     const bool ok = tile < f.ntiles && bn < f.nblocks;
-    load_raw<IT, NIN>(indices + (ok ? bn : 0) * (int64_t)NIN, ok, raw);
+    load_raw<IT, NIN>(indices + (ok ? bn : 0) * (int64_t)NIN, ok, idx32, raw);
     n_next = ok ? load_kind<FK>(maxima, bn) : 0.0;
   };
   if (REGPF && !stage_in) reg_prefetch(blockIdx.x);
@@ -232,7 +245,15 @@ k_fast_decompress(const FastParams p, const void* __restrict__ maxima,
         bool fast = false;
         if constexpr (row_vectorizable<TOut>(E)) fast = interior && f.vec_dense;
         if (fast) {
-          if constexpr (row_vectorizable<TOut>(E)) {
+          if constexpr ((E * sizeof(TOut)) % 32 == 0) {
+            if (f.vec32) {
+#pragma unroll
+              for (int r = 0; r < ROWS; ++r) store_row_vec32<TOut, E>(out + off + r * rs, v + r * E);
+            } else {
+#pragma unroll
+              for (int r = 0; r < ROWS; ++r) store_row_vec<TOut, E>(out + off + r * rs, v + r * E);
+            }
+          } else if constexpr (row_vectorizable<TOut>(E)) {
 #pragma unroll
             for (int r = 0; r < ROWS; ++r) store_row_vec<TOut, E>(out + off + r * rs, v + r * E);
           }
