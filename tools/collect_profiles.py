@@ -26,10 +26,12 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from ncu_summary import summarise  # noqa: E402
 
 OP_KERNELS = {  # bench op -> kernel name prefix
-    "compress": ("k_fast_compress", "k_half3_compress", "k_line3_compress", "k_exact_compress"),
-    "decompress": ("k_fast_decompress", "k_half3_decompress", "k_line3_decompress", "k_exact_decompress"),
-    "l2_norm": ("k_moments_vec", "k_moments_staged"),  # PAIR = 0 instantiation
-    "dot": ("k_moments_vec", "k_moments_staged"),      # PAIR = 1
+    "compress": ("k_dct8_compress", "k_fast_compress", "k_half3_compress", "k_line3_compress",
+                 "k_exact_compress"),
+    "decompress": ("k_dct8_decompress", "k_fast_decompress", "k_half3_decompress",
+                   "k_line3_decompress", "k_exact_decompress"),
+    "l2_norm": ("k_moments_stream", "k_moments_staged"),  # PAIR = false instantiation
+    "dot": ("k_moments_stream", "k_moments_staged"),      # PAIR = true
     "add": ("k_add",),
 }
 
@@ -110,8 +112,13 @@ def main():
             lines.append(f"{name[:58]:58s} {len(t):8d} {med / 1e3:10.1f} "
                          f"{(statistics.median(dram) / 1e6 if dram else 0):9.1f} {share:6.3f}")
             for op, prefixes in OP_KERNELS.items():
-                if op in ("l2_norm", "dot") and not name.endswith(", 0>" if op == "l2_norm" else ", 1>"):
-                    continue
+                targs = name[name.find("<") + 1:name.rfind(">")].split(", ") if "<" in name else []
+                if op in ("l2_norm", "dot") and "moments_stream" in name:
+                    pair = len(targs) > 3 and targs[3] in ("1", "true")
+                    if pair != (op == "dot"):
+                        continue
+                if op == "decompress" and targs and targs[-1] != "double":
+                    continue  # bench "decompress" is the f64-output call
                 if any(name.split("<")[0].endswith(p) or name.startswith("void " + p) or name.startswith(p)
                        for p in prefixes) and dram:
                     key = f"{w}:{op}"
