@@ -83,7 +83,8 @@ size_t bz_compress_workspace(const bz_layout* L) {
   Geo g = make_geo(L);
   size_t generic = exact_compress_workspace(g, g.nblocks);
   size_t convert = (size_t)dense_count(L) * float_kind_bytes(L->float_kind) + 256;
-  return std::max(std::max(generic, convert), dct8_compress_workspace(g)) + 256;
+  return std::max(std::max(generic, convert),
+                  std::max(dct8_compress_workspace(g), dct4_compress_workspace(g))) + 256;
 }
 
 int bz_compress(const bz_layout* L, const void* x, int x_kind, void* maxima, void* indices,
@@ -103,6 +104,9 @@ int bz_compress(const bz_layout* L, const void* x, int x_kind, void* maxima, voi
   if (!force_generic() && dct8_compress_supported(g, x_kind) && ws &&
       ws_bytes >= dct8_compress_workspace(g))
     return launch_dct8_compress(g, x, maxima, indices, ws, ws_bytes, s);
+  if (!force_generic() && dct4_compress_supported(g, x_kind) && ws &&
+      ws_bytes >= dct4_compress_workspace(g))
+    return launch_dct4_compress(g, x, maxima, indices, ws, ws_bytes, s);
   if (!force_generic() && fast_supported(g, x_kind))
     return launch_fast_compress(g, x, maxima, indices, s);
   return launch_exact_compress(g, x, x_kind, maxima, indices, nullptr, nullptr, g.nblocks, ws,
@@ -124,6 +128,9 @@ int bz_decompress(const bz_layout* L, const void* maxima, const void* indices, v
   if (!force_generic() && dct8_supported(g) && (out_kind == BZ_F64 || out_kind == BZ_F32) &&
       g.index_kind != BZ_I64)
     return launch_dct8_decompress(g, maxima, indices, out, out_kind, S(stream));
+  if (!force_generic() && dct4_supported(g) && (out_kind == BZ_F64 || out_kind == BZ_F32) &&
+      (g.index_kind == BZ_I8 || g.index_kind == BZ_I16))
+    return launch_dct4_decompress(g, maxima, indices, out, out_kind, S(stream));
   if (!force_generic() && fast_decompress_supported(g, out_kind))
     return launch_fast_decompress(g, maxima, indices, out, out_kind, S(stream));
   return launch_exact_decompress(g, maxima, indices, out, out_kind, ws, ws_bytes, S(stream));

@@ -1,0 +1,429 @@
+// bz_dct4.cu -- factored 4x4x4x4 DCT compress / decompress (the C5 path).
+//
+// Same scheme as bz_dct8.cu for 4-D blocks of 4^4 = 256 elements, any
+// pruning mask.  Each 4-point line uses the even/odd factorisation with the
+// row-0 entries of the reference matrix (transforms.py:67-71; rows 1-3 equal
+// them up to sign within 2 eps, measured), 3 FP64 ops per element and axis
+// instead of the reference's 4 FMAs, and no fixed axis order.
+//
+// Exactness of maxima and indices (codec.py:253-297):
+//   per axis and output, both the reference FMA chain (4u) and the
+//   butterflies (3u) plus the matrix perturbation (4u) stay within 11u of
+//   the exact product in units of (|H|^T |x|)_k; over four axes with
+//   |H| <= 0.654 and sum|x| <= 256 max|C| (Cauchy-Schwarz + Parseval):
+//   |C' - C_ref| <= 44u * 0.183 * 256 N <= 2^-41.9 N; we use delta = 2^-38 N'.
+//   The stored maximum round_to_kind(max|C|) must not depend on that
+//   uncertainty, and every KEPT coefficient's fixed-point fraction C'*r/N
+//   must be more than one 2^-24 unit from one half; otherwise (and for
+//   tiny / zero / non-finite maxima) the block is listed and recomputed by
+//   the exact generic kernel (bz_generic.cu, the reference FMA chain).
+//
+// Decompress: inverse butterflies with the scale N/r folded in first
+// (tolerance 1e-13 of the largest output, as bz_dct8.cu).
+//
+// Work decomposition: a warp owns two consecutive blocks (lanes 0-15 / 16-31)
+// and a private 2 x 2.1 KB shared region.  Lane o = (i1, i2) first owns the
+// (a0, a3) slice at a1 = i1, a2 = i2 -- four 16-byte rows from HBM, the two
+// blocks of a warp completing each 32-byte sector -- and transforms axes 0
+// and 3 in registers; after one warp-local exchange lane o = (k0, k3) owns
+// the (a1, a2) slice and transforms axes 1 and 2.  Kept coefficients go
+// through the rank table to a per-warp staging area and leave as one
+// contiguous run of 2K bytes per warp tile.
+#include "bz_fast.cuh"
+#include "bz_kernels.cuh"
+
+#include <cstdlib>
+
+namespace bz {
+
+namespace d4 {
+constexpr int BS = 256, NT = 256, WPC = NT / 32, BPW = 2;
+constexpr double kDeltaRel = 0x1p-38;
+
+// exchange layout: element (a0,a1,a2,a3) at 68*a0 + 17*a1 + 4*a2 + a3 (271
+// doubles per block, injective).  Both lane patterns -- (a1,a2) varying with
+// (a0,a3) fixed, and (a0,a3) varying with (a1,a2) fixed -- hit 16 distinct
+// 8-byte banks, and every access is a per-lane base plus an immediate.
+constexpr int XS = 272;  // doubles per block region
+__host__ __device__ constexpr int xoff(int a0, int a1, int a2, int a3) {
+  return 68 * a0 + 17 * a1 + 4 * a2 + a3;
+}
+constexpr int SS = BS + 16;  // staging bytes / elements per block (slot BS: zero)
+
+struct Dct4K {
+  double h00, a, c2, b;  // H[0][0], H[0][1], H[0][2], H[0][3]
+};
+__device__ __forceinline__ Dct4K dct4_consts(const double (&H)[64]) {
+  return Dct4K{H[0], H[1], H[2], H[3]};
+}
+
+// forward line (stride S): C[k] = sum_n x[n] H[n][k]
+template <int S>
+__device__ __forceinline__ void fdct4(double* v, const Dct4K& K) {
+  const double s0 = v[0] + v[3 * S], s1 = v[S] + v[2 * S];
+  const double d0 = v[0] - v[3 * S], d1 = v[S] - v[2 * S];
+  v[0] = K.h00 * (s0 + s1);
+  v[2 * S] = K.c2 * (s0 - s1);
+  v[S] = __fma_rn(K.a, d0, K.b * d1);
+  v[3 * S] = __fma_rn(K.b, d0, -K.a * d1);
+}
+
+// inverse line: x[n] = sum_k C[k] H[n][k]
+template <int S>
+__device__ __forceinline__ void idct4(double* v, const Dct4K& K) {
+  const double c0 = v[0], c1 = v[S], c2 = v[2 * S], c3 = v[3 * S];
+  const double h = K.h00 * c0;
+  const double e0 = __fma_rn(K.c2, c2, h), e1 = __fma_rn(-K.c2, c2, h);
+  const double o0 = __fma_rn(K.b, c3, K.a * c1), o1 = __fma_rn(-K.a, c3, K.b * c1);
+  v[0] = e0 + o0;
+  v[3 * S] = e0 - o0;
+  v[S] = e1 + o1;
+  v[2 * S] = e1 - o1;
+}
+}  // namespace d4
+
+// --------------------------------------------------------------- compress --
+template <int FK>
+__global__ void __launch_bounds__(256, 3)
+k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restrict__ maxima,
+                int8_t* __restrict__ indices, int32_t* __restrict__ list,
+                int32_t* __restrict__ count) {
+  using namespace d4;
+  const FastGeo& f = p.f;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int t = threadIdx.x;
+  const int lane = t & 31, w = t >> 5;
+  const int bs = lane >> 4, o = lane & 15;
+  double* blk = reinterpret_cast<double*>(smem_raw) + (w * BPW + bs) * XS;
+  int8_t* stg = reinterpret_cast<int8_t*>(reinterpret_cast<double*>(smem_raw) + WPC * BPW * XS) +
+                w * BPW * SS;  // per-warp output staging, 2 x (256 + 16) bytes
+  const int K = f.kept;
+  const Dct4K KC = dct4_consts(p.H);
+  // this lane's 16 output positions (k0 = o>>2, k3 = o&3, k1, k2) -> staging
+  // slot (rank; dropped coefficients go to the scratch slot BS)
+  const int k0 = o >> 2, k3 = o & 3;
+  int16_t rk[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int r_ = f.full_mask ? (k0 * 64 + q * 4 + k3) : f.rank[k0 * 64 + q * 4 + k3];
+    rk[q] = (int16_t)(r_ >= 0 ? r_ : BS);
+  }
+  const int i1 = o >> 2, i2 = o & 3;
+  double* wbase = blk + xoff(0, i1, i2, 0);  // phase A: (a0, a3) at immediates
+  double* rbase = blk + xoff(k0, 0, 0, k3);  // phase B: (a1, a2) at immediates
+  int8_t* sbase = stg + bs * SS;
+  const int64_t s0 = f.stride[0], s1 = f.stride[1], s2 = f.stride[2];
+  const int64_t nwt = (f.nblocks + BPW - 1) / BPW;
+
+  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += (int64_t)gridDim.x * WPC) {
+    const int64_t b = wt * BPW + bs;
+    const bool valid = b < f.nblocks;
+
+    // ---- A: (a0, a3) slice at (a1, a2) = (i1, i2); axes 0 and 3
+    double v[16];
+    {
+      int64_t gc[4] = {0, 0, 0, 0};
+      if (valid) block_coords<4>(f, b, gc);
+      const int64_t c0 = gc[0] * 4, c1 = gc[1] * 4 + i1, c2 = gc[2] * 4 + i2, c3 = gc[3] * 4;
+      const float* src = x + c0 * s0 + c1 * s1 + c2 * s2 + c3;
+      const bool full = valid && c0 + 4 <= f.shape[0] && c1 < f.shape[1] && c2 < f.shape[2] &&
+                        c3 + 4 <= f.shape[3];
+      if (full && f.vec_dense) {
+        uint4 r[4];
+#pragma unroll
+        for (int a0 = 0; a0 < 4; ++a0) r[a0] = __ldcs(reinterpret_cast<const uint4*>(src + a0 * s0));
+#pragma unroll
+        for (int a0 = 0; a0 < 4; ++a0) {
+          v[a0 * 4 + 0] = (double)__uint_as_float(r[a0].x);
+          v[a0 * 4 + 1] = (double)__uint_as_float(r[a0].y);
+          v[a0 * 4 + 2] = (double)__uint_as_float(r[a0].z);
+          v[a0 * 4 + 3] = (double)__uint_as_float(r[a0].w);
+        }
+      } else {
+        const bool ok12 = valid && c1 < f.shape[1] && c2 < f.shape[2];
+#pragma unroll
+        for (int a0 = 0; a0 < 4; ++a0)
+#pragma unroll
+          for (int a3 = 0; a3 < 4; ++a3)
+            v[a0 * 4 + a3] = (ok12 && c0 + a0 < f.shape[0] && c3 + a3 < f.shape[3])
+                                 ? (double)src[a0 * s0 + a3] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int a3 = 0; a3 < 4; ++a3) fdct4<4>(v + a3, KC);  // axis 0
+#pragma unroll
+    for (int a0 = 0; a0 < 4; ++a0) fdct4<1>(v + a0 * 4, KC);  // axis 3
+#pragma unroll
+    for (int a0 = 0; a0 < 4; ++a0)
+#pragma unroll
+      for (int a3 = 0; a3 < 4; ++a3) wbase[xoff(a0, 0, 0, a3)] = v[a0 * 4 + a3];
+    __syncwarp();
+    // ---- B: (a1, a2) slice at (k0, k3); axes 1 and 2
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = rbase[xoff(0, q >> 2, q & 3, 0)];
+    __syncwarp();
+#pragma unroll
+    for (int a2 = 0; a2 < 4; ++a2) fdct4<4>(v + a2, KC);  // axis 1
+#pragma unroll
+    for (int a1 = 0; a1 < 4; ++a1) fdct4<1>(v + a1 * 4, KC);  // axis 2
+    // v[k1*4 + k2] = C'[k0][k1][k2][k3]
+
+    // ---- block maximum (compare-select; non-finite -> N' = 0 or inf -> listed)
+    double m0 = 0.0, m1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; q += 2) {
+      const double a = fabs(v[q]), c = fabs(v[q + 1]);
+      m0 = a > m0 ? a : m0;
+      m1 = c > m1 ? c : m1;
+    }
+    double m = m1 > m0 ? m1 : m0;
+#pragma unroll
+    for (int sft = 8; sft > 0; sft >>= 1) {
+      const double a = __shfl_xor_sync(0xffffffffu, m, sft);
+      m = a > m ? a : m;
+    }
+    const double mx = m;
+    const double n = round_to_kind<FK>(mx);
+    const BinCtx bc = bin_ctx<false>(n, 127.0, mx);
+    bool bad = !bc.fast || !(mx < 1.7976931348623157e308) ||
+               round_to_kind<FK>(mx * (1.0 - kDeltaRel)) != round_to_kind<FK>(mx * (1.0 + kDeltaRel));
+
+    // ---- bin the kept coefficients (24-bit fixed point, as bz_dct8.cu)
+    unsigned zmin = 0xffffffffu;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int fx = __double2loint(__fma_rn(v[q], bc.R, 1.5 * 268435456.0));
+      const unsigned y1 = (unsigned)fx + (1u << 23) + 1u;
+      zmin = min(zmin, rk[q] < BS ? (y1 & 0xffffffu) : 0xffffffffu);  // kept coefficients only
+      sbase[rk[q]] = (int8_t)(y1 >> 24);
+    }
+    bad = bad || zmin <= 2u;
+    const unsigned badmask = __ballot_sync(0xffffffffu, bad && valid);
+    if (valid && o == 0) {
+      store_kind<FK>(maxima, b, n);
+      if ((badmask >> (bs * 16)) & 0xffffu) list[atomicAdd(count, 1)] = (int32_t)b;
+    }
+    __syncwarp();
+    // ---- the warp tile's kept indices: one contiguous run of nvalid * K bytes
+    {
+      const int64_t b0 = wt * BPW;
+      const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
+      const int nbytes = nv * K;
+      int8_t* dst = indices + b0 * (int64_t)K;
+      // the two staged blocks sit at stg[0..K) and stg[SS..SS+K)
+      if (((uintptr_t)dst & 3) == 0 && (K & 3) == 0) {
+        for (int i = lane; i < nbytes / 4; i += 32) {
+          const int e = i * 4;
+          const int blk_i = e / K, off = e - blk_i * K;
+          reinterpret_cast<uint32_t*>(dst)[i] = *reinterpret_cast<const uint32_t*>(stg + blk_i * SS + off);
+        }
+      } else if (((uintptr_t)dst & 3) == 0 && ((2 * K) & 3) == 0 && nv == BPW) {
+        // K = 2 mod 4 (e.g. 66): assemble words across the block seam
+        for (int i = lane; i < nbytes / 4; i += 32) {
+          uint32_t wd = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int e = i * 4 + j;
+            const int blk_i = e >= K, off = e - blk_i * K;
+            wd |= (uint32_t)(uint8_t)stg[blk_i * SS + off] << (8 * j);
+          }
+          reinterpret_cast<uint32_t*>(dst)[i] = wd;
+        }
+      } else {
+        for (int e = lane; e < nbytes; e += 32) {
+          const int blk_i = e >= K, off = e - blk_i * K;
+          dst[e] = stg[blk_i * SS + off];
+        }
+      }
+    }
+    __syncwarp();  // staging and exchange area reused by the next tile
+  }
+}
+
+// ------------------------------------------------------------- decompress --
+template <typename IT, int FK, typename TOut>
+__global__ void __launch_bounds__(256, 3)
+k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
+                  const IT* __restrict__ indices, TOut* __restrict__ out) {
+  using namespace d4;
+  const FastGeo& f = p.f;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int t = threadIdx.x;
+  const int lane = t & 31, w = t >> 5;
+  const int bs = lane >> 4, o = lane & 15;
+  double* blk = reinterpret_cast<double*>(smem_raw) + (w * BPW + bs) * XS;
+  IT* stg = reinterpret_cast<IT*>(reinterpret_cast<double*>(smem_raw) + WPC * BPW * XS) + w * BPW * SS;
+  const int K = f.kept;
+  const Dct4K KC = dct4_consts(p.H);
+  const int k0 = o >> 2, k3 = o & 3;
+  // staging slot of each of this lane's 16 coefficients; dropped ones read
+  // the zero slot BS (zeroed once, never written)
+  int16_t rk[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int r_ = f.full_mask ? (k0 * 64 + q * 4 + k3) : f.rank[k0 * 64 + q * 4 + k3];
+    rk[q] = (int16_t)(r_ >= 0 ? r_ : BS);
+  }
+  if (lane < 2) stg[lane * SS + BS] = (IT)0;
+  const int i1 = o >> 2, i2 = o & 3;
+  double* wbase = blk + xoff(k0, 0, 0, k3);
+  double* rbase = blk + xoff(0, i1, i2, 0);
+  const IT* sbase = stg + bs * SS;
+  const double rr = radius_f64(sizeof(IT) == 1 ? BZ_I8 : (sizeof(IT) == 2 ? BZ_I16 : BZ_I32));
+  const double rinv = 1.0 / rr;
+  const int64_t s0 = f.stride[0], s1 = f.stride[1], s2 = f.stride[2];
+  const int64_t nwt = (f.nblocks + BPW - 1) / BPW;
+
+  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += (int64_t)gridDim.x * WPC) {
+    const int64_t b = wt * BPW + bs;
+    const bool valid = b < f.nblocks;
+    // ---- the warp tile's kept indices -> staging (element granularity)
+    {
+      const int64_t b0 = wt * BPW;
+      const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
+      const IT* src = indices + b0 * (int64_t)K;
+      for (int e = lane; e < nv * K; e += 32) {
+        const int blk_i = e >= K, off = e - blk_i * K;
+        stg[blk_i * SS + off] = __ldcs(src + e);
+      }
+    }
+    const double nmax = valid ? load_kind<FK>(maxima, b) : 0.0;
+    const bool odd = !(nmax >= 0x1p-900 && nmax <= 0x1p+1000);
+    __syncwarp();
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = (double)sbase[rk[q]];
+#pragma unroll
+    for (int a2 = 0; a2 < 4; ++a2) idct4<4>(v + a2, KC);  // axis 1
+#pragma unroll
+    for (int a1 = 0; a1 < 4; ++a1) idct4<1>(v + a1 * 4, KC);  // axis 2
+    if (!odd) {
+      const double scale = nmax * rinv;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] *= scale;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) wbase[xoff(0, q >> 2, q & 3, 0)] = v[q];
+    __syncwarp();
+#pragma unroll
+    for (int a0 = 0; a0 < 4; ++a0)
+#pragma unroll
+      for (int a3 = 0; a3 < 4; ++a3) v[a0 * 4 + a3] = rbase[xoff(a0, 0, 0, a3)];
+    __syncwarp();
+#pragma unroll
+    for (int a3 = 0; a3 < 4; ++a3) idct4<4>(v + a3, KC);  // axis 0
+#pragma unroll
+    for (int a0 = 0; a0 < 4; ++a0) idct4<1>(v + a0 * 4, KC);  // axis 3
+    if (odd) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = __ddiv_rn(__dmul_rn(v[q], nmax), rr);
+    }
+    if (valid) {
+      int64_t gc[4] = {0, 0, 0, 0};
+      block_coords<4>(f, b, gc);
+      const int64_t c0 = gc[0] * 4, c1 = gc[1] * 4 + i1, c2 = gc[2] * 4 + i2, c3 = gc[3] * 4;
+      if (c1 < f.shape[1] && c2 < f.shape[2]) {
+        const bool full3 = c3 + 4 <= f.shape[3];
+        const int lim0 = (int)min((int64_t)4, f.shape[0] - c0);
+        TOut* base = out + c1 * s1 + c2 * s2 + c3;
+#pragma unroll
+        for (int a0 = 0; a0 < 4; ++a0) {
+          if (a0 < lim0) {
+            TOut* dst = base + (c0 + a0) * s0;
+            if (full3 && f.vec_dense) {
+              if constexpr (sizeof(TOut) == 8) {
+                if (f.vec32) store_row_vec32<TOut, 4>(dst, v + a0 * 4);
+                else store_row_vec<TOut, 4>(dst, v + a0 * 4);
+              } else {
+                store_row_vec<TOut, 4>(dst, v + a0 * 4);
+              }
+            } else {
+#pragma unroll
+              for (int a3 = 0; a3 < 4; ++a3)
+                if (c3 + a3 < f.shape[3]) dst[a3] = (TOut)v[a0 * 4 + a3];
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();  // staging and exchange area reused by the next tile
+  }
+}
+
+// ----------------------------------------------------------------- launch --
+bool dct4_supported(const Geo& g) {
+  if (g.ndim != 4 || g.transform != 0 || !g.matrices_host) return false;
+  for (int a = 0; a < 4; ++a)
+    if (g.block[a] != 4) return false;
+  if (g.float_kind != BZ_F32 && g.float_kind != BZ_F64) return false;
+  if (getenv("BZC_B200_EXACT")) return false;
+  return true;
+}
+
+bool dct4_compress_supported(const Geo& g, int x_kind) {
+  return dct4_supported(g) && g.index_kind == BZ_I8 && x_kind == BZ_F32 && g.float_kind == BZ_F32;
+}
+
+size_t dct4_compress_workspace(const Geo& g) { return 256 + (size_t)g.nblocks * sizeof(int32_t); }
+
+int launch_dct4_compress(const Geo& g, const void* x, void* maxima, void* indices, void* ws,
+                         size_t ws_bytes, cudaStream_t s) {
+  using namespace d4;
+  if (ws_bytes < dct4_compress_workspace(g)) { set_error("dct4 compress: workspace too small"); return BZ_E_WORKSPACE; }
+  FastParams p;
+  if (!make_fast_params(g, BPW * WPC, x, 4, p)) { set_error("dct4 compress: host matrices missing"); return BZ_E_INVALID; }
+  int32_t* count = reinterpret_cast<int32_t*>(ws);
+  int32_t* list = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(ws) + 256);
+  if (cudaMemsetAsync(count, 0, sizeof(int32_t), s) != cudaSuccess) return check_launch("dct4 memset");
+  const size_t smem = (size_t)WPC * BPW * XS * 8 + (size_t)WPC * BPW * SS;
+  auto kern = k_dct4_compress<BZ_F32>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+  const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));
+  kern<<<(int)grid, NT, smem, s>>>(p, reinterpret_cast<const float*>(x), maxima,
+                                   reinterpret_cast<int8_t*>(indices), list, count);
+  if (int rc = check_launch("dct4_compress")) return rc;
+  // exact fix-up of flagged blocks: the generic kernel (reference FMA chain)
+  return launch_exact_compress(g, x, BZ_F32, maxima, indices, list, count,
+                               std::min<int64_t>(g.nblocks, 4 * kSMs), nullptr, 0, s);
+}
+
+int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
+                           int out_kind, cudaStream_t s) {
+  using namespace d4;
+  FastParams p;
+  if (!make_fast_params(g, BPW * WPC, out, out_kind == BZ_F64 ? 8 : 4, p)) {
+    set_error("dct4 decompress: host matrices missing");
+    return BZ_E_INVALID;
+  }
+  const size_t smem = (size_t)WPC * BPW * XS * 8 + (size_t)WPC * BPW * SS * index_kind_bytes(g.index_kind);
+#define BZ_D(IT, FKV, TO)                                                                     \
+  {                                                                                           \
+    auto kern = k_dct4_decompress<IT, FKV, TO>;                                               \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    int occ = 1;                                                                              \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);                      \
+    const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));    \
+    kern<<<(int)grid, NT, smem, s>>>(p, maxima, reinterpret_cast<const IT*>(indices),         \
+                                     reinterpret_cast<TO*>(out));                             \
+    return check_launch("dct4_decompress");                                                   \
+  }
+#define BZ_O(IT, FKV)                           \
+  if (out_kind == BZ_F64) BZ_D(IT, FKV, double) \
+  if (out_kind == BZ_F32) BZ_D(IT, FKV, float)
+#define BZ_K(FKV)                                   \
+  switch (g.index_kind) {                           \
+    case BZ_I8: { BZ_O(int8_t, FKV) break; }        \
+    case BZ_I16: { BZ_O(int16_t, FKV) break; }      \
+  }
+  if (g.float_kind == BZ_F32) { BZ_K(BZ_F32) }
+  if (g.float_kind == BZ_F64) { BZ_K(BZ_F64) }
+#undef BZ_K
+#undef BZ_O
+#undef BZ_D
+  set_error("dct4 decompress: unsupported kinds");
+  return BZ_E_UNSUPPORTED;
+}
+
+}  // namespace bz

@@ -54,6 +54,15 @@ int launch_dct8_compress(const Geo& g, const void* x, void* maxima, void* indice
 int launch_dct8_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s);
 
+// factored 4x4x4x4 DCT with exact fix-up (bz_dct4.cu)
+bool dct4_supported(const Geo& g);
+bool dct4_compress_supported(const Geo& g, int x_kind);
+size_t dct4_compress_workspace(const Geo& g);
+int launch_dct4_compress(const Geo& g, const void* x, void* maxima, void* indices, void* ws,
+                         size_t ws_bytes, cudaStream_t s);
+int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
+                           int out_kind, cudaStream_t s);
+
 // compressed-domain ops (bz_ops.cu)
 int launch_negate(int ik, const void* in, void* out, int64_t n, cudaStream_t s);
 int launch_mul_scalar(const Geo& g, const void* maxima, const void* indices, double x,
