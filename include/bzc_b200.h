@@ -171,6 +171,19 @@ int bz_convert_indices(const void* in, int in_kind, void* out, int out_kind, int
 int bz_fill_random(void* out, int kind, int64_t n, int64_t offset, uint64_t seed, int dist,
                    void* stream);
 
+/* .bzc stream payload (format.py:108-127 serialize, 190-209 deserialize).
+ * The payload -- maxima bytes then index bytes, little-endian -- occupies
+ * stream bits [bit_offset, bit_offset + 8*(max_bytes+idx_bytes)); the host
+ * owns the header.  pack writes 32-bit words bit_offset/32 .. out_words-1 of
+ * `out` (4-byte aligned): the bits below bit_offset in the first word come
+ * from head_word, bits past the payload are zero (padding).  unpack reads
+ * `in_words` words of a stream (4-byte aligned) and fills both buffers. */
+int bz_stream_pack(const void* maxima, int64_t max_bytes, const void* indices, int64_t idx_bytes,
+                   int64_t bit_offset, uint32_t head_word, void* out, int64_t out_words,
+                   void* stream);
+int bz_stream_unpack(const void* in, int64_t in_words, int64_t bit_offset, void* maxima,
+                     int64_t max_bytes, void* indices, int64_t idx_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

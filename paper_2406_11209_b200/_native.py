@@ -84,6 +84,8 @@ SIGNATURES = {
     "bz_specified": (_I, [_L, _P, _P, _P, _P]),
     "bz_convert_indices": (_I, [_P, _I, _P, _I, _I64, _P]),
     "bz_fill_random": (_I, [_P, _I, _I64, _I64, ctypes.c_uint64, _I, _P]),
+    "bz_stream_pack": (_I, [_P, _I64, _P, _I64, _I64, ctypes.c_uint32, _P, _I64, _P]),
+    "bz_stream_unpack": (_I, [_P, _I64, _I64, _P, _I64, _P, _I64, _P]),
 }
 
 _lib = None

@@ -243,4 +243,17 @@ int bz_convert_indices(const void* in, int in_kind, void* out, int out_kind, int
   return launch_convert_indices(in, in_kind, out, out_kind, n, S(stream));
 }
 
+int bz_stream_pack(const void* maxima, int64_t max_bytes, const void* indices, int64_t idx_bytes,
+                   int64_t bit_offset, uint32_t head_word, void* out, int64_t out_words,
+                   void* stream) {
+  return launch_stream_pack(maxima, max_bytes, indices, idx_bytes, bit_offset, head_word, out,
+                            out_words, S(stream));
+}
+
+int bz_stream_unpack(const void* in, int64_t in_words, int64_t bit_offset, void* maxima,
+                     int64_t max_bytes, void* indices, int64_t idx_bytes, void* stream) {
+  return launch_stream_unpack(in, in_words, bit_offset, maxima, max_bytes, indices, idx_bytes,
+                              S(stream));
+}
+
 }  // extern "C"

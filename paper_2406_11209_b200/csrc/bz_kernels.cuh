@@ -63,6 +63,13 @@ int launch_dct4_compress(const Geo& g, const void* x, void* maxima, void* indice
 int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s);
 
+// .bzc stream payload (bz_format.cu)
+int launch_stream_pack(const void* maxima, int64_t max_bytes, const void* indices,
+                       int64_t idx_bytes, int64_t bit_offset, uint32_t head_word, void* out,
+                       int64_t out_words, cudaStream_t s);
+int launch_stream_unpack(const void* in, int64_t in_words, int64_t bit_offset, void* maxima,
+                         int64_t max_bytes, void* indices, int64_t idx_bytes, cudaStream_t s);
+
 // compressed-domain ops (bz_ops.cu)
 int launch_negate(int ik, const void* in, void* out, int64_t n, cudaStream_t s);
 int launch_mul_scalar(const Geo& g, const void* maxima, const void* indices, double x,
