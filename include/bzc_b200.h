@@ -171,6 +171,29 @@ int bz_convert_indices(const void* in, int in_kind, void* out, int out_kind, int
 int bz_fill_random(void* out, int kind, int64_t n, int64_t offset, uint64_t seed, int dist,
                    void* stream);
 
+/* block_means (ops.py:355-359): per-block mean F0*N/r/sqrt(bsize) in the
+ * reference's IEEE op order, row-major grid order, into out[nblocks] (f64). */
+int bz_block_means(const bz_layout* L, const void* maxima, const void* indices, double* out,
+                   void* stream);
+/* approx_wasserstein (ops.py:362-384) entirely on the device: block means,
+ * softmax where |sum - 1| > tol, radix sort, (mean |d|^order)^(1/order)
+ * into result[0] (device f64).  ws: bz_wasserstein_workspace(La) bytes. */
+size_t bz_wasserstein_workspace(const bz_layout* L);
+int bz_approx_wasserstein(const bz_layout* La, const bz_layout* Lb, const void* a_max,
+                          const void* a_idx, const void* b_max, const void* b_idx, double order,
+                          double tol, double* result, void* ws, size_t ws_bytes, void* stream);
+/* Fused time-series step (cli.py:240-243): the squared L2 norm of
+ * subtract(a, b) = add(a, negate(b)) -- sum over blocks of N^2 * sum q^2 with
+ * the rebinned q, N of the difference, bit-identical to materialising it --
+ * written to out[0] (device double) without writing the difference.  Returns
+ * BZ_E_UNSUPPORTED for configurations without a fused kernel (other index
+ * kinds, mixed float kinds, unaligned indices): compose bz_add + bz_moments.
+ * ws: bz_subtract_l2_workspace() bytes, zeroed before first use. */
+size_t bz_subtract_l2_workspace(void);
+int bz_subtract_l2(const bz_layout* La, const bz_layout* Lb, const void* a_max, const void* a_idx,
+                   const void* b_max, const void* b_idx, double* out, void* ws, size_t ws_bytes,
+                   void* stream);
+
 /* .bzc stream payload (format.py:108-127 serialize, 190-209 deserialize).
  * The payload -- maxima bytes then index bytes, little-endian -- occupies
  * stream bits [bit_offset, bit_offset + 8*(max_bytes+idx_bytes)); the host

@@ -105,12 +105,18 @@ __device__ __forceinline__ void st_max(void* p, int64_t i, double v, int fk) {
   else store_kind_rt(p, i, v, fk);
 }
 
-template <typename IT, int GS, int NCH, bool VEC, int FK, int MODE>
+// RED: instead of storing the result, accumulate its squared L2 norm
+// sum (q * N)^2 = sum_blocks N^2 * sum q^2 (exact integer block sums) and
+// reduce it deterministically into red_ws[1] (the fused time-series step
+// l2_norm(add(s[i+1], negate(s[i]))), cli.py:240-243, in one pass).
+template <typename IT, int GS, int NCH, bool VEC, int FK, int MODE, bool RED = false>
 __global__ void __launch_bounds__(256, 3)
 k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
       const void* __restrict__ a_max, const IT* __restrict__ a_idx,
       const void* __restrict__ b_max, const IT* __restrict__ b_idx, int subtract,
-      double shift, int mode_rt, void* __restrict__ out_max, IT* __restrict__ out_idx) {
+      double shift, int mode_rt, void* __restrict__ out_max, IT* __restrict__ out_idx,
+      double* __restrict__ red_ws = nullptr) {
+  double red_acc = 0.0;
   constexpr int mode = MODE;
   (void)mode_rt;
   constexpr int V = 16 / sizeof(IT);
@@ -207,8 +213,9 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
     }
     const double mx = __longlong_as_double((long long)key);  // NaN-propagating via bit order
     const double n = rnd_max<FK>(mx, fk_out);
-    if (sub == 0) st_max<FK>(out_max, b, n, fk_out);
+    if (!RED && sub == 0) st_max<FK>(out_max, b, n, fk_out);
     const BinCtx bc = bin_ctx(n, r, mx);
+    long long red_sq = 0;  // RED: this lane's exact sum of q^2 over the block
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       const int k0 = (ch * GS + sub) * V;
@@ -236,7 +243,13 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
           if (nr || !bc.fast || sizeof(IT) == 8) q64[e] = bin_exact_ctx(c[ch * V + e], bc, r, bound);
         }
       }
-      if (VEC && k0 < kept) {
+      if constexpr (RED) {
+        if constexpr (sizeof(IT) <= 2) {
+#pragma unroll
+          for (int e = 0; e < V; ++e)
+            if (VEC ? (k0 < kept) : (k0 + e < kept)) red_sq += (long long)(q[e] * q[e]);
+        }
+      } else if (VEC && k0 < kept) {
         if constexpr (sizeof(IT) <= 2) {
           __stcs(reinterpret_cast<uint4*>(out_idx + base + k0), pack16<IT>(q));
         } else {
@@ -261,6 +274,30 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
           }
         }
       }
+    }
+    if (RED) red_acc = __fma_rn((double)red_sq, n * n, red_acc);
+  }
+  if constexpr (RED) {
+    // deterministic: warp tree, CTA tree, last CTA sums the CTA partials in order
+    for (int o = 16; o > 0; o >>= 1) red_acc += __shfl_xor_sync(0xffffffffu, red_acc, o);
+    __shared__ double wsum[8];
+    __shared__ bool last;
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = red_acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += wsum[i];
+      red_ws[2 + blockIdx.x] = s;
+      __threadfence();
+      last = atomicAdd(reinterpret_cast<unsigned int*>(red_ws), 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      double s = 0.0;
+      for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(red_ws + 2 + i);
+      red_ws[1] = s;
+      *reinterpret_cast<unsigned int*>(red_ws) = 0u;  // re-arm
     }
   }
 }
@@ -316,6 +353,69 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
 #undef BZ_LAUNCH
 #undef BZ_K
   return check_launch("add");
+}
+
+// fused l2_norm(subtract(a, b)): the k_add RED variant; ws (zeroed once,
+// re-armed by the kernel) holds [counter, result, CTA partials]; the sum of
+// squares lands in ws[1] and is copied to `out`
+size_t subtract_l2_workspace() { return (size_t)(2 + kSMs * 3) * sizeof(double); }
+
+template <typename IT>
+static int launch_subtract_l2_t(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
+                                const void* b_max, const void* b_idx, double* ws, double* out,
+                                cudaStream_t s) {
+  constexpr int V = 16 / sizeof(IT);
+  const int kept = ga.kept;
+  const int vecs = (kept + V - 1) / V;
+  int GS = 1, NCH = 1;
+  if (vecs <= 4) {
+    NCH = vecs <= 1 ? 1 : (vecs <= 2 ? 2 : 4);
+  } else {
+    while (GS < 32 && GS < vecs) GS <<= 1;
+    NCH = (vecs + GS - 1) / GS;
+    if (NCH > 4) return BZ_E_UNSUPPORTED;
+    NCH = NCH <= 1 ? 1 : (NCH <= 2 ? 2 : 4);
+  }
+  const bool vec = ((kept * sizeof(IT)) % 16 == 0) && !(((uintptr_t)a_idx | (uintptr_t)b_idx) & 15);
+  if (!vec || ga.float_kind != gb.float_kind ||
+      (ga.float_kind != BZ_F32 && ga.float_kind != BZ_F64))
+    return BZ_E_UNSUPPORTED;
+  const int grid = grid_for(ga.nblocks * GS, 256, 3);
+#define BZ_R(G, N, F)                                                                          \
+  k_add<IT, G, N, true, F, 0, true><<<grid, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind,       \
+                                                         gb.float_kind, ga.float_kind, a_max,   \
+                                                         (const IT*)a_idx, b_max,               \
+                                                         (const IT*)b_idx, 1, 0.0, 0, nullptr,  \
+                                                         nullptr, ws)
+#define BZ_RF(G, N) \
+  do { if (ga.float_kind == BZ_F64) BZ_R(G, N, BZ_F64); else BZ_R(G, N, BZ_F32); } while (0)
+#define BZ_RG(G)                               \
+  case G:                                      \
+    if (NCH == 1) BZ_RF(G, 1);                 \
+    else if (NCH == 2) BZ_RF(G, 2);            \
+    else BZ_RF(G, 4);                          \
+    break;
+  switch (GS) { BZ_RG(1) BZ_RG(8) BZ_RG(16) BZ_RG(32) default: return BZ_E_UNSUPPORTED; }
+#undef BZ_RG
+#undef BZ_RF
+#undef BZ_R
+  if (int rc = check_launch("subtract_l2")) return rc;
+  if (cudaMemcpyAsync(out, ws + 1, sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return check_launch("subtract_l2 copy");
+  return BZ_OK;
+}
+
+int launch_subtract_l2(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
+                       const void* b_max, const void* b_idx, double* out, void* ws,
+                       size_t ws_bytes, cudaStream_t s) {
+  if (ws_bytes < subtract_l2_workspace()) { set_error("subtract_l2: workspace too small"); return BZ_E_WORKSPACE; }
+  if (ga.nblocks == 0 || ga.kept == 0) return cudaMemsetAsync(out, 0, sizeof(double), s) == cudaSuccess ? BZ_OK : BZ_E_CUDA;
+  double* w = reinterpret_cast<double*>(ws);
+  int rc = BZ_E_UNSUPPORTED;
+  if (ga.index_kind == BZ_I8) rc = launch_subtract_l2_t<int8_t>(ga, gb, a_max, a_idx, b_max, b_idx, w, out, s);
+  else if (ga.index_kind == BZ_I16) rc = launch_subtract_l2_t<int16_t>(ga, gb, a_max, a_idx, b_max, b_idx, w, out, s);
+  if (rc == BZ_E_UNSUPPORTED) set_error("subtract_l2: configuration not fused (use add + moments)");
+  return rc;
 }
 
 int launch_add(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,

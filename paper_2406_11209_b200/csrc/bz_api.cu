@@ -157,6 +157,18 @@ int bz_add(const bz_layout* La, const bz_layout* Lb, const void* a_max, const vo
                     out_max, out_idx, S(stream));
 }
 
+size_t bz_subtract_l2_workspace(void) { return subtract_l2_workspace(); }
+
+int bz_subtract_l2(const bz_layout* La, const bz_layout* Lb, const void* a_max, const void* a_idx,
+                   const void* b_max, const void* b_idx, double* out, void* ws, size_t ws_bytes,
+                   void* stream) {
+  if (int rc = validate(La)) return rc;
+  if (int rc = validate(Lb)) return rc;
+  if (La->index_kind != Lb->index_kind || La->kept != Lb->kept) { set_error("subtract_l2: incompatible operands"); return BZ_E_INVALID; }
+  return launch_subtract_l2(make_geo(La), make_geo(Lb), a_max, a_idx, b_max, b_idx, out, ws,
+                            ws_bytes, S(stream));
+}
+
 int bz_add_scalar(const bz_layout* L, const void* maxima, const void* indices, double shift,
                   void* out_max, void* out_idx, void* stream) {
   if (int rc = validate(L)) return rc;
@@ -241,6 +253,29 @@ int bz_fill_random(void* out, int kind, int64_t n, int64_t offset, uint64_t seed
 int bz_convert_indices(const void* in, int in_kind, void* out, int out_kind, int64_t n,
                        void* stream) {
   return launch_convert_indices(in, in_kind, out, out_kind, n, S(stream));
+}
+
+int bz_block_means(const bz_layout* L, const void* maxima, const void* indices, double* out,
+                   void* stream) {
+  if (int rc = validate(L)) return rc;
+  if (L->kept == 0 || !L->keeps_first) { set_error("block_means: mask drops the first coefficient"); return BZ_E_INVALID; }
+  return launch_block_means(make_geo(L), maxima, indices, out, S(stream));
+}
+
+size_t bz_wasserstein_workspace(const bz_layout* L) {
+  if (validate(L)) return 0;
+  return wasserstein_workspace(block_count(L));
+}
+
+int bz_approx_wasserstein(const bz_layout* La, const bz_layout* Lb, const void* a_max,
+                          const void* a_idx, const void* b_max, const void* b_idx, double order,
+                          double tol, double* result, void* ws, size_t ws_bytes, void* stream) {
+  if (int rc = validate(La)) return rc;
+  if (int rc = validate(Lb)) return rc;
+  if (block_count(La) != block_count(Lb)) { set_error("approx_wasserstein: block counts differ"); return BZ_E_INVALID; }
+  if (!La->keeps_first || !Lb->keeps_first || La->kept == 0 || Lb->kept == 0) { set_error("approx_wasserstein: mask drops the first coefficient"); return BZ_E_INVALID; }
+  return launch_approx_wasserstein(make_geo(La), make_geo(Lb), a_max, a_idx, b_max, b_idx, order,
+                                   tol, result, ws, ws_bytes, S(stream));
 }
 
 int bz_stream_pack(const void* maxima, int64_t max_bytes, const void* indices, int64_t idx_bytes,

@@ -63,6 +63,14 @@ int launch_dct4_compress(const Geo& g, const void* x, void* maxima, void* indice
 int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s);
 
+// block means / approximate Wasserstein distance (bz_wasserstein.cu)
+size_t wasserstein_workspace(int64_t nblocks);
+int launch_block_means(const Geo& g, const void* maxima, const void* indices, double* out,
+                       cudaStream_t s);
+int launch_approx_wasserstein(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
+                              const void* b_max, const void* b_idx, double order, double tol,
+                              double* result, void* ws, size_t ws_bytes, cudaStream_t s);
+
 // .bzc stream payload (bz_format.cu)
 int launch_stream_pack(const void* maxima, int64_t max_bytes, const void* indices,
                        int64_t idx_bytes, int64_t bit_offset, uint32_t head_word, void* out,
@@ -77,6 +85,10 @@ int launch_mul_scalar(const Geo& g, const void* maxima, const void* indices, dou
 int launch_add(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                const void* b_max, const void* b_idx, int subtract, double shift, int mode,
                void* out_max, void* out_idx, cudaStream_t s);
+size_t subtract_l2_workspace();
+int launch_subtract_l2(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
+                       const void* b_max, const void* b_idx, double* out, void* ws,
+                       size_t ws_bytes, cudaStream_t s);
 size_t moments_workspace(const Geo& g);
 int launch_moments(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                    const void* b_max, const void* b_idx, int pair, int dc_only, double* record,

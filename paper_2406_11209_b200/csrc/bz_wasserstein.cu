@@ -1,0 +1,307 @@
+// bz_wasserstein.cu -- block means and the approximate Wasserstein distance
+// (ops.py:351-384) on the device, no host round trip:
+//
+//   pa, pb = block_means(a), block_means(b)      F0*N/r/sqrt(bsize), IEEE order
+//   p <- softmax(p) if |sum p - 1| > tol          exp(p - max p) / sum
+//   d = |sort(pa) - sort(pb)|                     LSD radix sort, 8 x 8 bits
+//   W = (sum d^order / n)^(1/order)
+//
+// Reductions are two-stage and deterministic (fixed grid, partials summed in
+// CTA order).  The sort is a stable LSD radix sort of order-preserving 64-bit
+// keys: per pass a tile histogram, one exclusive scan, and a stable scatter
+// that ranks keys round by round (warp match + per-warp digit counts).
+#include "bz_common.cuh"
+#include "bz_kernels.cuh"
+
+#include <utility>
+
+namespace bz {
+
+namespace ws_ {
+constexpr int RT = 256;           // threads per CTA = keys per round
+constexpr int ROUNDS = 16;        // rounds per tile
+constexpr int TILE = RT * ROUNDS; // keys per tile
+constexpr int RED_CTAS = 296;     // partial-sum CTAs (fixed: deterministic)
+}  // namespace ws_
+
+// ------------------------------------------------------------ block means --
+template <typename IT>
+__global__ void k_block_means(int64_t nblocks, int kept, const void* __restrict__ maxima, int fk,
+                              const IT* __restrict__ indices, double r, double scale,
+                              double* __restrict__ out) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblocks;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const double f = (double)indices[b * (int64_t)kept];
+    const double n = load_kind_rt(maxima, b, fk);
+    // firsts = F0 * N; firsts /= r (ops.py:172-175); / block_mean_scale (ops.py:358)
+    out[b] = __ddiv_rn(__ddiv_rn(__dmul_rn(f, n), r), scale);
+  }
+}
+
+// ------------------------------------------- deterministic sum / max pass --
+// partial[c] = {sum a, max a, sum b, max b} over a fixed grid-stride slice
+__global__ void k_sum_max_partial(const double* __restrict__ a, const double* __restrict__ b,
+                                  int64_t n, double* __restrict__ partial) {
+  double sa = 0.0, sb = 0.0, ma = -INFINITY, mb = -INFINITY;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = a[i], y = b[i];
+    sa += x;
+    sb += y;
+    ma = fmax(ma, x);
+    mb = fmax(mb, y);
+  }
+  __shared__ double s[4][ws_::RT];
+  s[0][threadIdx.x] = sa; s[1][threadIdx.x] = ma; s[2][threadIdx.x] = sb; s[3][threadIdx.x] = mb;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s[0][threadIdx.x] += s[0][threadIdx.x + o];
+      s[1][threadIdx.x] = fmax(s[1][threadIdx.x], s[1][threadIdx.x + o]);
+      s[2][threadIdx.x] += s[2][threadIdx.x + o];
+      s[3][threadIdx.x] = fmax(s[3][threadIdx.x], s[3][threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 4; ++k) partial[blockIdx.x * 4 + k] = s[k][0];
+}
+
+// one CTA: stats = {sum a, max a, sum b, max b}
+__global__ void k_sum_max_final(const double* __restrict__ partial, int nparts,
+                                double* __restrict__ stats) {
+  if (threadIdx.x < 4) {
+    const int k = threadIdx.x;
+    double v = (k & 1) ? -INFINITY : 0.0;
+    for (int i = 0; i < nparts; ++i) v = (k & 1) ? fmax(v, partial[i * 4 + k]) : v + partial[i * 4 + k];
+    stats[k] = v;
+  }
+}
+
+// softmax step 1 (ops.py:351-353): x <- exp(x - max) where |sum - 1| > tol
+__global__ void k_softmax_exp(double* __restrict__ a, double* __restrict__ b, int64_t n,
+                              const double* __restrict__ stats, double tol,
+                              int* __restrict__ flags) {
+  const bool fa = fabs(stats[0] - 1.0) > tol, fb = fabs(stats[2] - 1.0) > tol;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { flags[0] = fa; flags[1] = fb; }
+  const double ma = stats[1], mb = stats[3];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (fa) a[i] = exp(a[i] - ma);
+    if (fb) b[i] = exp(b[i] - mb);
+  }
+}
+
+// softmax step 2: x <- x / sum x (stats recomputed after step 1)
+__global__ void k_softmax_div(double* __restrict__ a, double* __restrict__ b, int64_t n,
+                              const double* __restrict__ stats, const int* __restrict__ flags) {
+  const bool fa = flags[0], fb = flags[1];
+  const double sa = stats[0], sb = stats[2];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (fa) a[i] = __ddiv_rn(a[i], sa);
+    if (fb) b[i] = __ddiv_rn(b[i], sb);
+  }
+}
+
+// ------------------------------------------------------------ radix sort --
+__device__ __forceinline__ unsigned long long key_of(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);  // order-preserving
+}
+__device__ __forceinline__ double value_of(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+__global__ void k_to_keys(const double* __restrict__ x, unsigned long long* __restrict__ k, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    k[i] = key_of(x[i]);
+}
+
+// hist[d * ntiles + tile]
+__global__ void __launch_bounds__(ws_::RT)
+k_radix_hist(const unsigned long long* __restrict__ keys, int64_t n, int shift,
+             unsigned int* __restrict__ hist, int ntiles) {
+  __shared__ unsigned int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * ws_::TILE;
+  for (int rr = 0; rr < ws_::ROUNDS; ++rr) {
+    const int64_t i = base + rr * ws_::RT + threadIdx.x;
+    if (i < n) atomicAdd(&h[(unsigned)(keys[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// exclusive scan of m entries in place, one CTA of 1024 threads
+__global__ void __launch_bounds__(1024) k_scan_exclusive(unsigned int* __restrict__ v, int64_t m) {
+  __shared__ unsigned int part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (m + 1023) / 1024;
+  const int64_t s = t * per, e = min(m, s + per);
+  unsigned int sum = 0;
+  for (int64_t i = s; i < e; ++i) sum += v[i];
+  part[t] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
+    const unsigned int add = t >= o ? part[t - o] : 0u;
+    __syncthreads();
+    part[t] += add;
+    __syncthreads();
+  }
+  unsigned int run = t ? part[t - 1] : 0u;
+  for (int64_t i = s; i < e; ++i) {
+    const unsigned int x = v[i];
+    v[i] = run;
+    run += x;
+  }
+}
+
+// stable scatter: keys of tile `blockIdx.x` to their global positions
+__global__ void __launch_bounds__(ws_::RT)
+k_radix_scatter(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out,
+                int64_t n, int shift, const unsigned int* __restrict__ offsets, int ntiles) {
+  __shared__ unsigned int run[256];
+  __shared__ unsigned int wcnt[ws_::RT / 32][256];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  run[t] = offsets[(int64_t)t * ntiles + blockIdx.x];
+  for (int k = 0; k < ws_::RT / 32; ++k) wcnt[k][t] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * ws_::TILE;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int rr = 0; rr < ws_::ROUNDS; ++rr) {
+    const int64_t i = base + rr * ws_::RT + t;
+    const bool valid = i < n;
+    const unsigned long long key = valid ? in[i] : 0ull;
+    const unsigned d = valid ? ((unsigned)(key >> shift) & 255u) : 256u;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned lrank = __popc(peers & lt);
+    if (valid && lrank == 0) wcnt[w][d] = __popc(peers);
+    __syncthreads();
+    if (valid) {
+      unsigned pre = 0;
+      for (int w2 = 0; w2 < w; ++w2) pre += wcnt[w2][d];
+      out[run[d] + pre + lrank] = key;
+    }
+    __syncthreads();
+    unsigned tot = 0;
+    for (int k = 0; k < ws_::RT / 32; ++k) {
+      tot += wcnt[k][t];
+      wcnt[k][t] = 0;
+    }
+    run[t] += tot;
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------ order-p distance terms --
+__global__ void k_diff_pow_partial(const unsigned long long* __restrict__ ka,
+                                   const unsigned long long* __restrict__ kb, int64_t n, double p,
+                                   double* __restrict__ partial) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double dlt = fabs(value_of(ka[i]) - value_of(kb[i]));
+    s += p == 1.0 ? dlt : (p == 2.0 ? dlt * dlt : pow(dlt, p));
+  }
+  __shared__ double sh[ws_::RT];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k_diff_pow_final(const double* __restrict__ partial, int nparts, int64_t n,
+                                 double p, double* __restrict__ result) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < nparts; ++i) s += partial[i];
+    const double m = s / (double)n;
+    result[0] = p == 1.0 ? m : pow(m, 1.0 / p);
+  }
+}
+
+// ---------------------------------------------------------------- launch --
+static int64_t ntiles_of(int64_t n) { return (n + ws_::TILE - 1) / ws_::TILE; }
+
+size_t wasserstein_workspace(int64_t nblocks) {
+  const int64_t nt = ntiles_of(nblocks);
+  return 256 + (size_t)nblocks * 8 * 4        // pa, pb, two key buffers
+         + (size_t)256 * nt * 4 + 256         // histogram / offsets
+         + (size_t)ws_::RED_CTAS * 4 * 8 + 256;
+}
+
+int launch_block_means(const Geo& g, const void* maxima, const void* indices, double* out,
+                       cudaStream_t s) {
+  const double r = radius_f64(g.index_kind), scale = sqrt((double)g.bsize);
+  const int grid = grid_for(g.nblocks, 256, 8);
+  switch (g.index_kind) {
+    case BZ_I8: k_block_means<int8_t><<<grid, 256, 0, s>>>(g.nblocks, g.kept, maxima, g.float_kind, (const int8_t*)indices, r, scale, out); break;
+    case BZ_I16: k_block_means<int16_t><<<grid, 256, 0, s>>>(g.nblocks, g.kept, maxima, g.float_kind, (const int16_t*)indices, r, scale, out); break;
+    case BZ_I32: k_block_means<int32_t><<<grid, 256, 0, s>>>(g.nblocks, g.kept, maxima, g.float_kind, (const int32_t*)indices, r, scale, out); break;
+    default: k_block_means<int64_t><<<grid, 256, 0, s>>>(g.nblocks, g.kept, maxima, g.float_kind, (const int64_t*)indices, r, scale, out); break;
+  }
+  return check_launch("block_means");
+}
+
+static int radix_sort(unsigned long long* keys, unsigned long long* tmp, int64_t n,
+                      unsigned int* hist, cudaStream_t s) {
+  const int nt = (int)ntiles_of(n);
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 8 * pass;
+    k_radix_hist<<<nt, ws_::RT, 0, s>>>(keys, n, shift, hist, nt);
+    k_scan_exclusive<<<1, 1024, 0, s>>>(hist, (int64_t)256 * nt);
+    k_radix_scatter<<<nt, ws_::RT, 0, s>>>(keys, tmp, n, shift, hist, nt);
+    if (int rc = check_launch("radix pass")) return rc;
+    std::swap(keys, tmp);  // 8 passes: the result ends in the original buffer
+  }
+  return BZ_OK;
+}
+
+int launch_approx_wasserstein(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
+                              const void* b_max, const void* b_idx, double order, double tol,
+                              double* result, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int64_t n = ga.nblocks;
+  if (ws_bytes < wasserstein_workspace(n)) { set_error("approx_wasserstein: workspace too small"); return BZ_E_WORKSPACE; }
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws);
+  auto take = [&](size_t bytes) { unsigned char* q = p; p += (bytes + 255) / 256 * 256; return q; };
+  double* pa = reinterpret_cast<double*>(take(n * 8));
+  double* pb = reinterpret_cast<double*>(take(n * 8));
+  unsigned long long* ka = reinterpret_cast<unsigned long long*>(pa);  // keys replace values
+  unsigned long long* kb = reinterpret_cast<unsigned long long*>(pb);
+  unsigned long long* t1 = reinterpret_cast<unsigned long long*>(take(n * 8));
+  unsigned long long* t2 = reinterpret_cast<unsigned long long*>(take(n * 8));
+  unsigned int* hist = reinterpret_cast<unsigned int*>(take((size_t)256 * ntiles_of(n) * 4));
+  double* partial = reinterpret_cast<double*>(take((size_t)ws_::RED_CTAS * 4 * 8));
+  double* stats = reinterpret_cast<double*>(take(64));
+  int* flags = reinterpret_cast<int*>(stats + 4);
+  if (n == 0) {  // mean over no blocks: NaN, as the reference's 0/0
+    k_diff_pow_final<<<1, 32, 0, s>>>(partial, 0, 0, order, result);
+    return check_launch("wasserstein empty");
+  }
+  if (int rc = launch_block_means(ga, a_max, a_idx, pa, s)) return rc;
+  if (int rc = launch_block_means(gb, b_max, b_idx, pb, s)) return rc;
+  const int g = grid_for(n, ws_::RT, 8);
+  k_sum_max_partial<<<ws_::RED_CTAS, ws_::RT, 0, s>>>(pa, pb, n, partial);
+  k_sum_max_final<<<1, 32, 0, s>>>(partial, ws_::RED_CTAS, stats);
+  k_softmax_exp<<<g, ws_::RT, 0, s>>>(pa, pb, n, stats, tol, flags);
+  k_sum_max_partial<<<ws_::RED_CTAS, ws_::RT, 0, s>>>(pa, pb, n, partial);
+  k_sum_max_final<<<1, 32, 0, s>>>(partial, ws_::RED_CTAS, stats);
+  k_softmax_div<<<g, ws_::RT, 0, s>>>(pa, pb, n, stats, flags);
+  k_to_keys<<<g, ws_::RT, 0, s>>>(pa, ka, n);
+  k_to_keys<<<g, ws_::RT, 0, s>>>(pb, kb, n);
+  if (int rc = check_launch("wasserstein prep")) return rc;
+  if (int rc = radix_sort(ka, t1, n, hist, s)) return rc;
+  if (int rc = radix_sort(kb, t2, n, hist, s)) return rc;
+  k_diff_pow_partial<<<ws_::RED_CTAS, ws_::RT, 0, s>>>(ka, kb, n, order, partial);
+  k_diff_pow_final<<<1, 32, 0, s>>>(partial, ws_::RED_CTAS, n, order, result);
+  return check_launch("wasserstein distance");
+}
+
+}  // namespace bz

@@ -45,6 +45,11 @@ __all__ = [
     "cosine_similarity",
     "ssim",
     "ssim_components",
+    "WassersteinParams",
+    "block_means",
+    "approx_wasserstein",
+    "subtract_l2",
+    "timeseries_distances",
     "Record",
     "moments_record",
     "merge_records",
@@ -410,3 +415,126 @@ def ssim(a: CompressedArray, b: CompressedArray, params: SsimParams | None = Non
     return (_signed_power(lum, params.luminance_weight, "luminance")
             * _signed_power(con, params.contrast_weight, "contrast")
             * _signed_power(st, params.structure_weight, "structure"))
+
+
+# ------------------------------------------------ time-series workflow --
+_SL2_WS: dict = {}
+
+
+def _subtract_l2_sq(a: CompressedArray, b: CompressedArray, out: torch.Tensor) -> bool:
+    """Squared L2 norm of subtract(a, b) into the device double ``out`` with
+    the fused kernel (bz_subtract_l2); False when no fused kernel serves the
+    configuration (the caller composes subtract + l2_norm, also on the GPU)."""
+    _check_compatible(a, b, index_kind=True)
+    dev = a.device
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    nbytes = _native.query("bz_subtract_l2_workspace")
+    ws = _SL2_WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        _SL2_WS[key] = ws
+    La, Lb = a.layout(), b.layout()
+    bi = b.indices if b.device == dev else b.indices.to(dev)
+    bm = b.maxima if b.device == dev else b.maxima.to(dev)
+    rc = _native.query("bz_subtract_l2", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
+                       a.indices.data_ptr(), bm.data_ptr(), bi.data_ptr(), out.data_ptr(),
+                       ws.data_ptr(), ws.numel(), _stream(a))
+    if rc == -2:  # BZ_E_UNSUPPORTED
+        return False
+    if rc != 0:
+        raise _native.NativeError(f"bz_subtract_l2 failed ({rc}): "
+                                  f"{_native.load_library().bz_last_error().decode()}")
+    return True
+
+
+def subtract_l2(a: CompressedArray, b: CompressedArray) -> float:
+    """l2_norm(subtract(a, b)) in one fused pass (cli.py:240-243); the same
+    value as materialising the difference (rebinned under a's settings)."""
+    if getattr(a, "_reduce_record", None) is not None:  # sharded: compose
+        return l2_norm(subtract(a, b))
+    out = torch.empty(1, dtype=torch.float64, device=a.device)
+    if not _subtract_l2_sq(a, b, out):
+        return l2_norm(subtract(a, b))
+    return float(math.sqrt(max(float(out.item()), 0.0))) / _radius(a)
+
+
+def timeseries_distances(snapshots, measure: str = "l2", p: float = 1.0) -> list:
+    """Distances between consecutive snapshots, the reference CLI's
+    ``timeseries-diff`` (cli.py:225-259): ``l2`` = l2_norm(add(s[i+1],
+    negate(s[i]))) (fused, one pass per pair, one host read for all pairs);
+    ``wasserstein`` = approx_wasserstein(s[i], s[i+1]) of order p."""
+    snaps = list(snapshots)
+    if len(snaps) < 2:
+        return []
+    if measure == "wasserstein":
+        params = WassersteinParams(order=p)
+        return [approx_wasserstein(snaps[i], snaps[i + 1], params) for i in range(len(snaps) - 1)]
+    if measure != "l2":
+        raise ValueError(f"unknown measure {measure!r}")
+    n = len(snaps) - 1
+    out = torch.empty(n, dtype=torch.float64, device=snaps[0].device)
+    dists: list = [None] * n
+    for i in range(n):
+        if getattr(snaps[i + 1], "_reduce_record", None) is not None or \
+                not _subtract_l2_sq(snaps[i + 1], snaps[i], out[i:i + 1]):
+            dists[i] = l2_norm(subtract(snaps[i + 1], snaps[i]))
+    host = out.cpu().numpy()
+    r = _radius(snaps[0])
+    return [d if d is not None else float(math.sqrt(max(float(host[i]), 0.0))) / r
+            for i, d in enumerate(dists)]
+
+
+# ------------------------------------------ block means / Wasserstein --
+@dataclass(frozen=True)
+class WassersteinParams:
+    """Order and normalization tolerance for the approximate distance (ops.py:87-97)."""
+
+    order: float = 1.0
+    normalization_tolerance: float = 1e-6
+
+    def __post_init__(self):
+        if not self.order >= 1.0:
+            raise ValueError(f"order must be >= 1, got {self.order}")
+        if self.normalization_tolerance < 0:
+            raise ValueError("normalization tolerance must be non-negative")
+
+
+def block_means(a: CompressedArray) -> torch.Tensor:
+    """Per-block means, flattened in row-major grid order (ops.py:355-359):
+    F0 * N / r / sqrt(block size), the reference's op order; f64 on the GPU."""
+    _require_first_coefficient(a)
+    out = torch.empty(a.block_count, dtype=torch.float64, device=a.device)
+    La = a.layout()
+    _native.call("bz_block_means", ctypes.byref(La), a.maxima.data_ptr(), a.indices.data_ptr(),
+                 out.data_ptr(), _stream(a))
+    return out
+
+
+_WS_W: dict = {}
+
+
+def approx_wasserstein(a: CompressedArray, b: CompressedArray,
+                       params: WassersteinParams | None = None) -> float:
+    """Order-p distance between the sorted block-mean distributions
+    (ops.py:362-384): block means, softmax where they do not sum to 1, device
+    radix sort, (mean |d|^p)^(1/p) -- one host read of the result."""
+    params = params or WassersteinParams()
+    _check_compatible(a, b)
+    _require_first_coefficient(a)
+    _require_first_coefficient(b)
+    dev = a.device
+    La, Lb = a.layout(), b.layout()
+    nbytes = _native.query("bz_wasserstein_workspace", ctypes.byref(La))
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    ws = _WS_W.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        _WS_W[key] = ws
+    bi = b.indices if b.device == dev else b.indices.to(dev)
+    bm = b.maxima if b.device == dev else b.maxima.to(dev)
+    res = torch.empty(1, dtype=torch.float64, device=dev)
+    _native.call("bz_approx_wasserstein", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
+                 a.indices.data_ptr(), bm.data_ptr(), bi.data_ptr(), float(params.order),
+                 float(params.normalization_tolerance), res.data_ptr(), ws.data_ptr(), ws.numel(),
+                 _stream(a))
+    return float(res.item())
