@@ -40,7 +40,7 @@ __device__ __forceinline__ Rec rec_merge(const Rec& x, const Rec& y) {
   }
   Rec r;
   r.n = x.n + y.n;
-  const double inv = 1.0 / r.n;
+  const double inv = __drcp_rn(r.n);  // == 1.0 / n, without the division sequence
   const double da = y.ma - x.ma, db = y.mb - x.mb;
   const double wy = y.n * inv, f = x.n * y.n * inv;
   r.ma = x.ma + da * wy;
@@ -134,7 +134,7 @@ struct MomState {
     Rec r = rec_zero();
     r.n = cnt;
     if (cnt > 0 && dc) {
-      const double inv = 1.0 / cnt;
+      const double inv = __drcp_rn(cnt);
       r.ma = pa + sa * inv;
       r.mb = pb + sb * inv;
       r.Mab = sab - sa * sb * inv;

@@ -112,18 +112,17 @@ def serialize_to_device(a: CompressedArray) -> torch.Tensor:
     dev = a.device
     out = torch.empty(nwords * 4, dtype=torch.uint8, device=dev)
     # whole header words on the host; the partial word goes to the kernel
-    hw = np.zeros(nwords * 32, dtype=np.uint8)
+    full = P // 32
+    hw = np.zeros((full + 1) * 32, dtype=np.uint8)
     hw[:P] = head
     words = np.packbits(hw, bitorder="little").view("<u4")
-    full = P // 32
     if full:
-        out[: full * 4].copy_(torch.from_numpy(words[:full].view(np.uint8).copy()))
+        out[: full * 4].copy_(torch.from_numpy(words[:full].view(np.uint8).copy()), non_blocking=True)
     maxima = a.maxima.contiguous()
     indices = a.indices.contiguous()
     _native.call("bz_stream_pack", maxima.data_ptr(), maxima.numel() * maxima.element_size(),
                  indices.data_ptr(), indices.numel() * indices.element_size(), P,
-                 int(words[full]) if full < nwords else 0, out.data_ptr(), nwords,
-                 _native.stream_handle(dev))
+                 int(words[full]), out.data_ptr(), nwords, _native.stream_handle(dev))
     return out[:total]
 
 

@@ -51,6 +51,8 @@ CONFIGS = {
     "c2": ((8192, 8192), (4, 4), "f64", "i16", None),
     "c3": ((1024, 1024, 1024), (8, 8, 8), "f32", "i8", None),
     "c5": ((256, 256, 256, 64), (4, 4, 4, 4), "f32", "i8", "lowpass"),
+    "c4": ((1024, 1024, 1024), (8, 8, 8), "f32", "i8", None),  # uniform data (dist 1)
+    "c2x4": ((16384, 16384), (4, 4), "f64", "i16", None),      # tail-cost probe
 }
 
 
@@ -60,8 +62,9 @@ def run(name):
     s = bz.CodecSettings(block, bz.FloatKind(fk), bz.IndexKind(ik),
                          mask=None if bits is None else bz.PruningMask(block, bits))
     kind = bz.FloatKind(fk)
-    x = fill(shape, kind, 1, 0)
-    y = fill(shape, kind, 2, 0)
+    dist = 1 if name == "c4" else 0
+    x = fill(shape, kind, 1, dist)
+    y = fill(shape, kind, 2, dist)
     n = x.values.numel()
     inb = n * kind.itemsize
     B = int(np.prod(s.grid_for(shape)))
@@ -84,6 +87,13 @@ def run(name):
     rec("negate", timeit(lambda: bz.negate(ca)), 2 * B * K * s.index_kind.itemsize)
     rec("l2_norm(api)", timeit(lambda: bz.l2_norm(ca)), comp_bytes)
     rec("mean(api)", timeit(lambda: bz.mean(ca)), B * (s.index_kind.itemsize + kind.itemsize))
+    if s.mask.keeps_first:
+        rec("cov(api)", timeit(lambda: bz.covariance(ca, cb)), 2 * comp_bytes, 2 * inb)
+        rec("ssim(api)", timeit(lambda: bz.ssim(ca, cb)), 2 * comp_bytes, 2 * inb)
+        rec("subtract_l2", timeit(lambda: bz.subtract_l2(cb, ca)), 2 * comp_bytes, 2 * inb)
+        rec("wasserstein", timeit(lambda: bz.approx_wasserstein(ca, cb), reps=3, warm=1),
+            2 * B * (s.index_kind.itemsize + kind.itemsize))
+    rec("serialize_dev", timeit(lambda: bz.serialize_to_device(ca)), 2 * comp_bytes)
     print(f"== {name} shape={shape} block={block} {fk}/{ik} K={K} fast={bz.is_fast_path(s, shape)}")
     for op, ms, g_in, g_alg, frac in rows:
         print(f"  {op:16s} {ms*1e3:9.1f} us  in {g_in:8.0f} GB/s  alg {g_alg:7.0f} GB/s  frac {frac:.3f}")
