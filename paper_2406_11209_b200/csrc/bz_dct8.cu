@@ -47,19 +47,38 @@ constexpr double kDeltaRel = 0x1p-37;
 
 // Each warp owns two blocks (lanes 0-15 / 16-31) and a private 2 x 4 KB
 // shared region; block-local positions are moved as 16-byte units u (pairs of
-// doubles) with the swizzle u ^ ((u>>3 ^ u>>6) & 7), which makes all three
-// access patterns below (z-rows, y-columns, x-rows) conflict-free per
-// quarter warp.
-__device__ __forceinline__ int swz(int pos) {
-  const int u = pos >> 1;
-  return ((u ^ (((u >> 3) ^ (u >> 6)) & 7)) << 1);
+// doubles, u = z*32 + y*4 + x/2) with the swizzle u ^ ((u>>3 ^ u>>6) & 7),
+// which makes all three access patterns (z-rows, y-columns, x-rows)
+// conflict-free per quarter warp.  For each pattern the swizzled unit splits
+// into a per-lane part and a compile-time part joined by XOR in the low three
+// bits, so each lane precomputes the eight addresses base + ((c ^ k) << 4)
+// (k = 0..7) once; every access is then one of them plus an immediate:
+//   A  (lane y, h; access z, jj):  c = 2h ^ 4(y&1) ^ (y>>1), k = jj ^ 4(z&1) ^ (z>>1),
+//                                  + (y>>1)*8 units (lane) + z*32 (imm)
+//   B  (lane kz, h; access yy, jj): c = 2h ^ 4(kz&1) ^ (kz>>1), k = jj ^ 4(yy&1) ^ (yy>>1),
+//                                  + kz*32 (lane) + (yy>>1)*8 (imm)
+//   C  (lane kz, h; access i, xu):  same c as B, k = xu ^ 4(i&1) ^ (i>>1),
+//                                  + kz*32 + 16h (lane) + (i>>1)*8 (imm)
+struct Lut8 {
+  unsigned a[8];
+};
+__device__ __forceinline__ Lut8 lut8(unsigned base, int c) {
+  Lut8 L;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) L.a[k] = base + ((unsigned)(c ^ k) << 4);
+  return L;
 }
-__device__ __forceinline__ void st2(double* blk, int pos, double a, double b) {
-  *reinterpret_cast<double2*>(blk + swz(pos)) = make_double2(a, b);
+__device__ __forceinline__ void sts2(unsigned addr, double a, double b) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(a), "d"(b) : "memory");
 }
-__device__ __forceinline__ double2 ld2(const double* blk, int pos) {
-  return *reinterpret_cast<const double2*>(blk + swz(pos));
+__device__ __forceinline__ double2 lds2(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
 }
+__host__ __device__ constexpr int kA(int z, int jj) { return jj ^ (4 * (z & 1)) ^ (z >> 1); }
+__host__ __device__ constexpr int kB(int yy, int jj) { return jj ^ (4 * (yy & 1)) ^ (yy >> 1); }
+__host__ __device__ constexpr int kC(int i, int xu) { return xu ^ (4 * (i & 1)) ^ (i >> 1); }
 
 // The 8-point DCT-II matrix has eight distinct magnitudes: H[n][0] = H00 and,
 // for k > 0, |H[n][k]| = c_m = 0.5 cos(m pi / 16) for some m.  Every entry is
@@ -132,6 +151,11 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
   const int64_t s0 = f.stride[0], s1 = f.stride[1];
   const int64_t nwt = (f.nblocks + BPW - 1) / BPW;  // warp tiles
   const Dct8K KC = dct8_consts(p.H);
+  const unsigned bbase = (unsigned)__cvta_generic_to_shared(blk);
+  // phase A: lane (y = hi, h); phases B, C: lane (kz = hi, h)
+  const Lut8 LA = lut8(bbase + (unsigned)((hi >> 1) * 8) * 16u, (2 * h) ^ (4 * (hi & 1)) ^ (hi >> 1));
+  const Lut8 LB = lut8(bbase + (unsigned)(hi * 32) * 16u, (2 * h) ^ (4 * (hi & 1)) ^ (hi >> 1));
+  const unsigned cofs = (unsigned)(16 * h) * 16u;  // phase C lane offset
 
   // the next warp tile's rows are prefetched (cp.async) into per-thread
   // staging slots ([row][thread], conflict-free) while this tile computes
@@ -201,7 +225,7 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
 #pragma unroll
     for (int z = 0; z < 8; ++z)
 #pragma unroll
-      for (int j = 0; j < 4; j += 2) st2(blk, z * 64 + hi * 8 + h * 4 + j, v[z * 4 + j], v[z * 4 + j + 1]);
+      for (int j = 0; j < 4; j += 2) sts2(LA.a[kA(z, j >> 1)] + z * 32 * 16, v[z * 4 + j], v[z * 4 + j + 1]);
     __syncwarp();
 
     // ---- B: thread (kz = hi, x half h): 8 y x 4 x, axis 1
@@ -209,7 +233,7 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
     for (int yy = 0; yy < 8; ++yy)
 #pragma unroll
       for (int j = 0; j < 4; j += 2) {
-        const double2 q = ld2(blk, hi * 64 + yy * 8 + h * 4 + j);
+        const double2 q = lds2(LB.a[kB(yy, j >> 1)] + (yy >> 1) * 8 * 16);
         v[yy * 4 + j] = q.x;
         v[yy * 4 + j + 1] = q.y;
       }
@@ -219,7 +243,7 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
 #pragma unroll
     for (int yy = 0; yy < 8; ++yy)
 #pragma unroll
-      for (int j = 0; j < 4; j += 2) st2(blk, hi * 64 + yy * 8 + h * 4 + j, v[yy * 4 + j], v[yy * 4 + j + 1]);
+      for (int j = 0; j < 4; j += 2) sts2(LB.a[kB(yy, j >> 1)] + (yy >> 1) * 8 * 16, v[yy * 4 + j], v[yy * 4 + j + 1]);
     __syncwarp();
 
     // ---- C: rows ky = 4h..4h+3 of 8 x, axis 2
@@ -228,7 +252,7 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int xx = 0; xx < 8; xx += 2) {
-        const double2 q = ld2(blk, hi * 64 + (4 * h + i) * 8 + xx);
+        const double2 q = lds2(LB.a[kC(i, xx >> 1)] + cofs + (i >> 1) * 8 * 16);
         c[i * 8 + xx] = q.x;
         c[i * 8 + xx + 1] = q.y;
       }
@@ -363,6 +387,11 @@ k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
   const int hi = o >> 1, h = o & 1;
   double* blk = reinterpret_cast<double*>(smem_raw) + (w * BPW + bs) * BS;
   const Dct8K KC = dct8_consts(p.H);
+  const unsigned bbase = (unsigned)__cvta_generic_to_shared(blk);
+  // phase A: lane (y = hi, h); phases B, C: lane (kz = hi, h)
+  const Lut8 LA = lut8(bbase + (unsigned)((hi >> 1) * 8) * 16u, (2 * h) ^ (4 * (hi & 1)) ^ (hi >> 1));
+  const Lut8 LB = lut8(bbase + (unsigned)(hi * 32) * 16u, (2 * h) ^ (4 * (hi & 1)) ^ (hi >> 1));
+  const unsigned cofs = (unsigned)(16 * h) * 16u;  // phase C lane offset
   const double rr = radius_f64(sizeof(IT) == 1 ? BZ_I8 : (sizeof(IT) == 2 ? BZ_I16 : BZ_I32));
   const double rinv = 1.0 / rr;
   const int64_t s0 = f.stride[0], s1 = f.stride[1];
@@ -408,14 +437,14 @@ k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int xx = 0; xx < 8; xx += 2) st2(blk, hi * 64 + (4 * h + i) * 8 + xx, c[i * 8 + xx], c[i * 8 + xx + 1]);
+      for (int xx = 0; xx < 8; xx += 2) sts2(LB.a[kC(i, xx >> 1)] + cofs + (i >> 1) * 8 * 16, c[i * 8 + xx], c[i * 8 + xx + 1]);
     __syncwarp();
     double* v = c;
 #pragma unroll
     for (int yy = 0; yy < 8; ++yy)
 #pragma unroll
       for (int j = 0; j < 4; j += 2) {
-        const double2 q = ld2(blk, hi * 64 + yy * 8 + h * 4 + j);
+        const double2 q = lds2(LB.a[kB(yy, j >> 1)] + (yy >> 1) * 8 * 16);
         v[yy * 4 + j] = q.x;
         v[yy * 4 + j + 1] = q.y;
       }
@@ -425,7 +454,7 @@ k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
 #pragma unroll
     for (int yy = 0; yy < 8; ++yy)
 #pragma unroll
-      for (int j = 0; j < 4; j += 2) st2(blk, hi * 64 + yy * 8 + h * 4 + j, v[yy * 4 + j], v[yy * 4 + j + 1]);
+      for (int j = 0; j < 4; j += 2) sts2(LB.a[kB(yy, j >> 1)] + (yy >> 1) * 8 * 16, v[yy * 4 + j], v[yy * 4 + j + 1]);
     __syncwarp();
 
     // ---- A': thread (y = hi, x half h): 8 kz x 4 x, axis 0 -> rows z
@@ -433,7 +462,7 @@ k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
     for (int z = 0; z < 8; ++z)
 #pragma unroll
       for (int j = 0; j < 4; j += 2) {
-        const double2 q = ld2(blk, z * 64 + hi * 8 + h * 4 + j);
+        const double2 q = lds2(LA.a[kA(z, j >> 1)] + z * 32 * 16);
         v[z * 4 + j] = q.x;
         v[z * 4 + j + 1] = q.y;
       }
