@@ -255,19 +255,21 @@ __device__ __forceinline__ unsigned word_mask(int p_bytes, int w) {
 }
 
 // exact sums of the chunk's elements [0, p) (segment 0) and [p, V) (segment 1)
-template <typename IT, bool PAIR, int NW>
+template <typename IT, bool PAIR, int NW, bool SPAN = true>
 __device__ __forceinline__ void seg_sums(SegSums<IT>& s, const Chunk<NW>& a, const Chunk<NW>& b,
                                          int p) {
   constexpr int V = NW * 4 / (int)sizeof(IT);
   if constexpr (sizeof(IT) == 1) {
     int a0 = 0, ab0 = 0, b0 = 0, a1 = 0, ab1 = 0, b1 = 0;
-    if (p >= V) {
+    // warp-uniform choice (the seam path is branch-free and also right for
+    // p >= V, where its mask is all ones): no divergent double execution
+    if (!SPAN || __all_sync(__activemask(), p >= V)) {  // no active lane at a block seam
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
         a0 = __dp4a((int)a.w[w], (int)a.w[w], a0);
         if (PAIR) { ab0 = __dp4a((int)a.w[w], (int)b.w[w], ab0); b0 = __dp4a((int)b.w[w], (int)b.w[w], b0); }
       }
-    } else {
+    } else {  // branch-free two-segment split (p >= V: the mask is all ones)
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
         const unsigned m = word_mask(p, w);
@@ -415,7 +417,7 @@ k_moments_stream(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
   auto consume = [&](const ChunkPos& cp, const Chunk<NW>& wa, const Chunk<NW>& wb, const Nm& n) {
     const int p = SPAN ? kept - cp.off : V;  // elements of block cp.b in this chunk = min(p, V)
     SegSums<IT> s;
-    seg_sums<IT, PAIR, NW>(s, wa, wb, p);
+    seg_sums<IT, PAIR, NW, SPAN>(s, wa, wb, p);
     if (cp.off == 0) {  // block b starts here: element 0 is its DC
       const long long x0 = chunk_elem<IT, NW>(wa, 0), y0 = PAIR ? chunk_elem<IT, NW>(wb, 0) : x0;
       if (dc) {
