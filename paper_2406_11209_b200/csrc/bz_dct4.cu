@@ -50,31 +50,38 @@ __host__ __device__ constexpr int xoff(int a0, int a1, int a2, int a3) {
 }
 constexpr int SS = BS + 16;  // staging bytes / elements per block (slot BS: zero)
 
+// The even entries are 1/2 (H[0][0] = 0.5, H[0][2] = 0.5 + 1 ulp), so each
+// line is evaluated scaled by exactly 2: even outputs need no multiply, the
+// odd constants are 2*H[0][1] and 2*H[0][3] (exact doublings).  After the
+// four axes every value carries the exact factor 16, folded into the
+// maximum, the binning scale and the decompress scale (powers of two: the
+// rounding is unchanged; the 1-ulp change of the even entries is inside the
+// error bound above).
 struct Dct4K {
-  double h00, a, c2, b;  // H[0][0], H[0][1], H[0][2], H[0][3]
+  double a2, b2;  // 2*H[0][1], 2*H[0][3]
 };
 __device__ __forceinline__ Dct4K dct4_consts(const double (&H)[64]) {
-  return Dct4K{H[0], H[1], H[2], H[3]};
+  return Dct4K{2.0 * H[1], 2.0 * H[3]};
 }
+constexpr double kUnscale = 0.0625;  // 1 / 2^4
 
-// forward line (stride S): C[k] = sum_n x[n] H[n][k]
+// forward line (stride S), times 2: 2 C[k] = 2 sum_n x[n] H[n][k]
 template <int S>
 __device__ __forceinline__ void fdct4(double* v, const Dct4K& K) {
   const double s0 = v[0] + v[3 * S], s1 = v[S] + v[2 * S];
   const double d0 = v[0] - v[3 * S], d1 = v[S] - v[2 * S];
-  v[0] = K.h00 * (s0 + s1);
-  v[2 * S] = K.c2 * (s0 - s1);
-  v[S] = __fma_rn(K.a, d0, K.b * d1);
-  v[3 * S] = __fma_rn(K.b, d0, -K.a * d1);
+  v[0] = s0 + s1;
+  v[2 * S] = s0 - s1;
+  v[S] = __fma_rn(K.a2, d0, K.b2 * d1);
+  v[3 * S] = __fma_rn(K.b2, d0, -K.a2 * d1);
 }
 
-// inverse line: x[n] = sum_k C[k] H[n][k]
+// inverse line, times 2: 2 x[n] = 2 sum_k C[k] H[n][k]
 template <int S>
 __device__ __forceinline__ void idct4(double* v, const Dct4K& K) {
   const double c0 = v[0], c1 = v[S], c2 = v[2 * S], c3 = v[3 * S];
-  const double h = K.h00 * c0;
-  const double e0 = __fma_rn(K.c2, c2, h), e1 = __fma_rn(-K.c2, c2, h);
-  const double o0 = __fma_rn(K.b, c3, K.a * c1), o1 = __fma_rn(-K.a, c3, K.b * c1);
+  const double e0 = c0 + c2, e1 = c0 - c2;
+  const double o0 = __fma_rn(K.b2, c3, K.a2 * c1), o1 = __fma_rn(-K.a2, c3, K.b2 * c1);
   v[0] = e0 + o0;
   v[3 * S] = e0 - o0;
   v[S] = e1 + o1;
@@ -182,9 +189,10 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
       const double a = __shfl_xor_sync(0xffffffffu, m, sft);
       m = a > m ? a : m;
     }
-    const double mx = m;
+    const double mx = m * kUnscale;  // values carry the factor 16
     const double n = round_to_kind<FK>(mx);
     const BinCtx bc = bin_ctx<false>(n, 127.0, mx);
+    const double R16 = bc.R * kUnscale;
     bool bad = !bc.fast || !(mx < 1.7976931348623157e308) ||
                round_to_kind<FK>(mx * (1.0 - kDeltaRel)) != round_to_kind<FK>(mx * (1.0 + kDeltaRel));
 
@@ -192,7 +200,7 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
     unsigned zmin = 0xffffffffu;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-      const int fx = __double2loint(__fma_rn(v[q], bc.R, 1.5 * 268435456.0));
+      const int fx = __double2loint(__fma_rn(v[q], R16, 1.5 * 268435456.0));
       const unsigned y1 = (unsigned)fx + (1u << 23) + 1u;
       zmin = min(zmin, rk[q] < BS ? (y1 & 0xffffffu) : 0xffffffffu);  // kept coefficients only
       sbase[rk[q]] = (int8_t)(y1 >> 24);
@@ -298,7 +306,7 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
 #pragma unroll
     for (int a1 = 0; a1 < 4; ++a1) idct4<1>(v + a1 * 4, KC);  // axis 2
     if (!odd) {
-      const double scale = nmax * rinv;
+      const double scale = nmax * rinv * kUnscale;
 #pragma unroll
       for (int q = 0; q < 16; ++q) v[q] *= scale;
     }
@@ -316,7 +324,7 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
     for (int a0 = 0; a0 < 4; ++a0) idct4<1>(v + a0 * 4, KC);  // axis 3
     if (odd) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = __ddiv_rn(__dmul_rn(v[q], nmax), rr);
+      for (int q = 0; q < 16; ++q) v[q] = __ddiv_rn(__dmul_rn(v[q] * kUnscale, nmax), rr);
     }
     if (valid) {
       int64_t gc[4] = {0, 0, 0, 0};
