@@ -122,23 +122,50 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
   const int64_t s0 = f.stride[0], s1 = f.stride[1], s2 = f.stride[2];
   const int64_t nwt = (f.nblocks + BPW - 1) / BPW;
 
-  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += (int64_t)gridDim.x * WPC) {
+  // the next warp tile's rows are prefetched (cp.async) into per-lane
+  // staging slots ([row][thread]) while this tile computes
+  uint4* pre = reinterpret_cast<uint4*>(smem_raw + (size_t)WPC * BPW * XS * 8 + (size_t)WPC * BPW * SS);
+  const int64_t wstride = (int64_t)gridDim.x * WPC;
+  auto rows_src = [&](int64_t wt_, const float*& src, int64_t (&gc)[4]) -> bool {
+    const int64_t b_ = wt_ * BPW + bs;
+    const bool ok = wt_ < nwt && b_ < f.nblocks;
+    gc[0] = gc[1] = gc[2] = gc[3] = 0;
+    if (ok) block_coords<4>(f, b_, gc);
+    const int64_t c0 = gc[0] * 4, c1 = gc[1] * 4 + i1, c2 = gc[2] * 4 + i2, c3 = gc[3] * 4;
+    src = x + c0 * s0 + c1 * s1 + c2 * s2 + c3;
+    return ok && f.vec_dense && c0 + 4 <= f.shape[0] && c1 < f.shape[1] && c2 < f.shape[2] &&
+           c3 + 4 <= f.shape[3];
+  };
+  auto prefetch = [&](int64_t wt_) -> bool {
+    const float* src;
+    int64_t gc[4];
+    const bool full = rows_src(wt_, src, gc);
+    if (full) {
+#pragma unroll
+      for (int a0 = 0; a0 < 4; ++a0) cp_async16(pre + a0 * NT + t, src + a0 * s0);
+    }
+    cp_async_commit();
+    return full;
+  };
+  bool staged = prefetch(blockIdx.x * (int64_t)WPC + w);
+
+  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += wstride) {
     const int64_t b = wt * BPW + bs;
     const bool valid = b < f.nblocks;
 
     // ---- A: (a0, a3) slice at (a1, a2) = (i1, i2); axes 0 and 3
     double v[16];
     {
-      int64_t gc[4] = {0, 0, 0, 0};
-      if (valid) block_coords<4>(f, b, gc);
+      const float* src;
+      int64_t gc[4];
+      rows_src(wt, src, gc);
       const int64_t c0 = gc[0] * 4, c1 = gc[1] * 4 + i1, c2 = gc[2] * 4 + i2, c3 = gc[3] * 4;
-      const float* src = x + c0 * s0 + c1 * s1 + c2 * s2 + c3;
-      const bool full = valid && c0 + 4 <= f.shape[0] && c1 < f.shape[1] && c2 < f.shape[2] &&
-                        c3 + 4 <= f.shape[3];
-      if (full && f.vec_dense) {
+      if (staged) {
+        cp_async_wait_all();
         uint4 r[4];
 #pragma unroll
-        for (int a0 = 0; a0 < 4; ++a0) r[a0] = __ldcs(reinterpret_cast<const uint4*>(src + a0 * s0));
+        for (int a0 = 0; a0 < 4; ++a0) r[a0] = pre[a0 * NT + t];
+        staged = prefetch(wt + wstride);  // own slots, already read
 #pragma unroll
         for (int a0 = 0; a0 < 4; ++a0) {
           v[a0 * 4 + 0] = (double)__uint_as_float(r[a0].x);
@@ -147,6 +174,7 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
           v[a0 * 4 + 3] = (double)__uint_as_float(r[a0].w);
         }
       } else {
+        staged = prefetch(wt + wstride);
         const bool ok12 = valid && c1 < f.shape[1] && c2 < f.shape[2];
 #pragma unroll
         for (int a0 = 0; a0 < 4; ++a0)
@@ -383,7 +411,7 @@ int launch_dct4_compress(const Geo& g, const void* x, void* maxima, void* indice
   int32_t* count = reinterpret_cast<int32_t*>(ws);
   int32_t* list = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(ws) + 256);
   if (cudaMemsetAsync(count, 0, sizeof(int32_t), s) != cudaSuccess) return check_launch("dct4 memset");
-  const size_t smem = (size_t)WPC * BPW * XS * 8 + (size_t)WPC * BPW * SS;
+  const size_t smem = (size_t)WPC * BPW * XS * 8 + (size_t)WPC * BPW * SS + (size_t)4 * NT * 16;
   auto kern = k_dct4_compress<BZ_F32>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 1;
