@@ -153,29 +153,13 @@ class _Reader:
         return int(sum(int(b) << j for j, b in enumerate(bits)))
 
 
-def deserialize(data) -> CompressedArray:
-    """Decode a stream (bytes, bytearray, numpy uint8 or a uint8 tensor).
-
-    The header is parsed on the host; the payload is unpacked on the GPU.
-    Raises TruncatedStream, InvalidTypeCode or ZeroExtent on malformed input
-    (format.py:165-209), before any device work.
-    """
-    if isinstance(data, torch.Tensor):
-        stream = data.reshape(-1)
-        if stream.dtype != torch.uint8:
-            raise TypeError("stream tensor must be uint8")
-        host_head = stream[:1 << 20].cpu().numpy()
-        nbytes = stream.numel()
-    else:
-        buf = np.frombuffer(bytes(data), dtype=np.uint8)
-        stream = None
-        host_head = buf[:1 << 20]
-        nbytes = buf.size
-    r = _Reader(host_head, nbytes * 8)
-    fk_code = r.uint(2)
-    ik_code = r.uint(2)
-    float_kind = FloatKind.from_code(fk_code)
-    index_kind = IndexKind.from_code(ik_code)
+def parse_header(head: np.ndarray, total_bytes: int):
+    """Parse a stream's header on the host (format.py:165-188): returns
+    (shape, CodecSettings, payload bit offset).  Raises TruncatedStream,
+    InvalidTypeCode or ZeroExtent exactly as the reference."""
+    r = _Reader(np.asarray(head, dtype=np.uint8), total_bytes * 8)
+    float_kind = FloatKind.from_code(r.uint(2))
+    index_kind = IndexKind.from_code(r.uint(2))
     transform_code = r.uint(8)
     if transform_code not in (0, 1):
         raise InvalidTypeCode(f"unknown transform code {transform_code}")
@@ -198,13 +182,37 @@ def deserialize(data) -> CompressedArray:
     P = r.pos
     grid = settings.grid_for(tuple(shape))
     blocks = math.prod(grid)
-    kept = mask.kept_count
-    max_bytes = blocks * float_kind.itemsize
-    idx_bytes = blocks * kept * index_kind.itemsize
-    if P + 8 * (max_bytes + idx_bytes) > nbytes * 8:
-        raise TruncatedStream(
-            f"needed {8 * (max_bytes + idx_bytes)} payload bits at offset {P}, "
-            f"stream has {nbytes * 8}")
+    payload_bits = 8 * blocks * (float_kind.itemsize + mask.kept_count * index_kind.itemsize)
+    if P + payload_bits > total_bytes * 8:
+        raise TruncatedStream(f"needed {payload_bits} payload bits at offset {P}, "
+                              f"stream has {total_bytes * 8}")
+    return tuple(shape), settings, P
+
+
+def deserialize(data) -> CompressedArray:
+    """Decode a stream (bytes, bytearray, numpy uint8 or a uint8 tensor).
+
+    The header is parsed on the host; the payload is unpacked on the GPU.
+    Raises TruncatedStream, InvalidTypeCode or ZeroExtent on malformed input
+    (format.py:165-209), before any device work.
+    """
+    if isinstance(data, torch.Tensor):
+        stream = data.reshape(-1)
+        if stream.dtype != torch.uint8:
+            raise TypeError("stream tensor must be uint8")
+        host_head = stream[:1 << 20].cpu().numpy()
+        nbytes = stream.numel()
+    else:
+        buf = np.frombuffer(bytes(data), dtype=np.uint8)
+        stream = None
+        host_head = buf[:1 << 20]
+        nbytes = buf.size
+    shape, settings, P = parse_header(host_head, nbytes)
+    grid = settings.grid_for(shape)
+    blocks = math.prod(grid)
+    kept = settings.mask.kept_count
+    max_bytes = blocks * settings.float_kind.itemsize
+    idx_bytes = blocks * kept * settings.index_kind.itemsize
     dev = stream.device if (stream is not None and stream.is_cuda) else _device()
     nwords = (nbytes + 3) // 4
     words = torch.zeros(nwords * 4, dtype=torch.uint8, device=dev)
@@ -212,8 +220,8 @@ def deserialize(data) -> CompressedArray:
         words[:nbytes].copy_(stream)
     else:
         words[:nbytes].copy_(torch.from_numpy(buf.copy()))
-    maxima = torch.empty(grid, dtype=float_kind.torch_dtype, device=dev)
-    indices = torch.empty(tuple(grid) + (kept,), dtype=index_kind.torch_dtype, device=dev)
+    maxima = torch.empty(grid, dtype=settings.float_kind.torch_dtype, device=dev)
+    indices = torch.empty(tuple(grid) + (kept,), dtype=settings.index_kind.torch_dtype, device=dev)
     _native.call("bz_stream_unpack", words.data_ptr(), nwords, P, maxima.data_ptr(), max_bytes,
                  indices.data_ptr(), idx_bytes, _native.stream_handle(dev))
-    return CompressedArray(tuple(shape), settings, maxima, indices)
+    return CompressedArray(shape, settings, maxima, indices)
