@@ -194,6 +194,18 @@ int bz_subtract_l2(const bz_layout* La, const bz_layout* Lb, const void* a_max, 
                    const void* b_max, const void* b_idx, double* out, void* ws, size_t ws_bytes,
                    void* stream);
 
+/* Error predictors (metrics.py:108-124), one value per block (f64):
+ * bin_bound = N/(2r+1), loose_linf = max|C| * prod(i), l2_coeff =
+ * sqrt(sum (Chat - C)^2) with Chat = (F*N)/r; coeffs = the true coefficient
+ * blocks (nblocks x prod(i), row-major). */
+int bz_error_bounds(const bz_layout* L, const void* maxima, const void* indices,
+                    const double* coeffs, double* bin_bound, double* loose_linf, double* l2_coeff,
+                    void* stream);
+/* Round-trip errors (metrics.py:127-148): per block sum (x - y)^2 and
+ * max |x - y| of two blocked f64 arrays. */
+int bz_block_diff(int64_t nblocks, int bsize, const double* x, const double* y, double* l2sq,
+                  double* maxabs, void* stream);
+
 /* .bzc stream payload (format.py:108-127 serialize, 190-209 deserialize).
  * The payload -- maxima bytes then index bytes, little-endian -- occupies
  * stream bits [bit_offset, bit_offset + 8*(max_bytes+idx_bytes)); the host

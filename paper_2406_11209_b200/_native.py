@@ -89,6 +89,8 @@ SIGNATURES = {
     "bz_approx_wasserstein": (_I, [_L, _L, _P, _P, _P, _P, _D, _D, _P, _P, _SZ, _P]),
     "bz_subtract_l2_workspace": (_SZ, []),
     "bz_subtract_l2": (_I, [_L, _L, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "bz_error_bounds": (_I, [_L, _P, _P, _P, _P, _P, _P, _P]),
+    "bz_block_diff": (_I, [_I64, _I, _P, _P, _P, _P, _P]),
     "bz_stream_pack": (_I, [_P, _I64, _P, _I64, _I64, ctypes.c_uint32, _P, _I64, _P]),
     "bz_stream_unpack": (_I, [_P, _I64, _I64, _P, _I64, _P, _I64, _P]),
 }

@@ -278,6 +278,20 @@ int bz_approx_wasserstein(const bz_layout* La, const bz_layout* Lb, const void* 
                                    tol, result, ws, ws_bytes, S(stream));
 }
 
+int bz_error_bounds(const bz_layout* L, const void* maxima, const void* indices,
+                    const double* coeffs, double* bin_bound, double* loose_linf, double* l2_coeff,
+                    void* stream) {
+  if (int rc = validate(L)) return rc;
+  return launch_error_bounds(make_geo(L), maxima, indices, coeffs, bin_bound, loose_linf, l2_coeff,
+                             S(stream));
+}
+
+int bz_block_diff(int64_t nblocks, int bsize, const double* x, const double* y, double* l2sq,
+                  double* maxabs, void* stream) {
+  if (nblocks < 0 || bsize < 1) { set_error("block_diff: bad sizes"); return BZ_E_INVALID; }
+  return launch_block_diff(nblocks, bsize, x, y, l2sq, maxabs, S(stream));
+}
+
 int bz_stream_pack(const void* maxima, int64_t max_bytes, const void* indices, int64_t idx_bytes,
                    int64_t bit_offset, uint32_t head_word, void* out, int64_t out_words,
                    void* stream) {

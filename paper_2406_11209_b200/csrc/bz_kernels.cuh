@@ -71,6 +71,13 @@ int launch_approx_wasserstein(const Geo& ga, const Geo& gb, const void* a_max, c
                               const void* b_max, const void* b_idx, double order, double tol,
                               double* result, void* ws, size_t ws_bytes, cudaStream_t s);
 
+// error predictors (bz_metrics.cu)
+int launch_error_bounds(const Geo& g, const void* maxima, const void* indices,
+                        const double* coeffs, double* bin_bound, double* loose_linf,
+                        double* l2_coeff, cudaStream_t s);
+int launch_block_diff(int64_t nblocks, int bsize, const double* x, const double* y, double* l2sq,
+                      double* maxabs, cudaStream_t s);
+
 // .bzc stream payload (bz_format.cu)
 int launch_stream_pack(const void* maxima, int64_t max_bytes, const void* indices,
                        int64_t idx_bytes, int64_t bit_offset, uint32_t head_word, void* out,

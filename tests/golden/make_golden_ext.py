@@ -26,6 +26,7 @@ sys.path.insert(0, os.environ.get("BZC_REFERENCE_SRC", "/root/reference/pkg/src"
 import bzc  # noqa: E402
 from bzc import ops as bops  # noqa: E402
 from bzc.format import serialize  # noqa: E402
+from bzc import metrics as bmetrics  # noqa: E402
 from bzc.kinds import FloatKind, IndexKind  # noqa: E402
 
 FK = {k.value: k for k in FloatKind}
@@ -79,6 +80,7 @@ def main():
         bits = mask_bits(mspec, block)
         s = bzc.CodecSettings(block, FK[fk], IK[ik], mask=bzc.PruningMask.from_bits(block, bits))
         xs = [data(dkind, shape, rng) for _ in range(3)]
+        arrays[f"{name}/x0"] = xs[0]
         cs = [bzc.compress(bzc.DenseArray.of(x, FK[fk]), s) for x in xs]
         p = f"{name}/"
         arrays[p + "mask"] = bits
@@ -96,6 +98,17 @@ def main():
             entry["wasserstein"] = w
             entry["timeseries_l2"] = [float(bops.l2_norm(bops.add(cs[i + 1], bops.negate(cs[i]))))
                                       for i in range(2)]
+        if dkind != "nan":
+            rep = bmetrics.measure_roundtrip(bzc.DenseArray.of(xs[0], FK[fk]), s)
+            arrays[p + "bin_bound"] = np.asarray(rep.per_block_bin_bound, dtype=np.float64)
+            arrays[p + "loose_linf"] = np.asarray(rep.per_block_loose_linf, dtype=np.float64)
+            arrays[p + "l2_coeff"] = np.asarray(rep.per_block_l2_coeff_error, dtype=np.float64)
+            arrays[p + "obs_l2_blocks"] = np.asarray(rep.per_block_observed_l2, dtype=np.float64)
+            entry["observed_linf"] = rep.observed_linf
+            entry["observed_l2"] = rep.observed_l2
+            nbytes = len(serialize(cs[0]))
+            entry["ratio"] = [bmetrics.compression_ratio(32, s, shape),
+                              bmetrics.measured_ratio(32, shape, nbytes), nbytes]
         table.append(entry)
     # Wasserstein on block means that already sum to 1 (no softmax): 1-element blocks
     s1 = bzc.CodecSettings((1, 1), FloatKind.F64, IndexKind.I32)

@@ -102,3 +102,34 @@ def test_fused_subtract_l2_c3_slab(bz):
     fused = bz.subtract_l2(xs[1], xs[0])
     comp = bz.l2_norm(bz.subtract(xs[1], xs[0]))
     assert math.isclose(fused, comp, rel_tol=1e-12)
+
+
+METRIC_CASES = [c for c in TABLE if c.get("observed_linf") is not None]
+
+
+@pytest.mark.parametrize("case", METRIC_CASES, ids=lambda c: c["name"])
+def test_error_report_matches_reference(bz, case):
+    """per-block predictors and round-trip errors on the GPU
+    vs bzc.metrics.measure_roundtrip; ratios vs bzc.metrics."""
+    from paper_2406_11209_b200 import metrics
+
+    name = case["name"]
+    block = tuple(case["block"])
+    s = bz.CodecSettings(block, bz.FloatKind(case["float_kind"]), bz.IndexKind(case["index_kind"]),
+                         mask=bz.PruningMask(block, ARR[f"{name}/mask"]))
+    x = ARR[f"{name}/x0"]
+    rep = metrics.measure_roundtrip(bz.DenseArray.of(x, bz.FloatKind(case["float_kind"])), s)
+    assert np.array_equal(rep.per_block_bin_bound.cpu().numpy(), ARR[f"{name}/bin_bound"])
+    assert np.array_equal(rep.per_block_loose_linf.cpu().numpy(), ARR[f"{name}/loose_linf"])
+    np.testing.assert_allclose(rep.per_block_l2_coeff_error.cpu().numpy(), ARR[f"{name}/l2_coeff"],
+                               rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(rep.per_block_observed_l2.cpu().numpy(), ARR[f"{name}/obs_l2_blocks"],
+                               rtol=1e-9, atol=1e-300)
+    assert math.isclose(rep.observed_linf, case["observed_linf"], rel_tol=1e-9, abs_tol=1e-300)
+    assert math.isclose(rep.observed_l2, case["observed_l2"], rel_tol=1e-9, abs_tol=1e-300)
+    closed, measured, nbytes = case["ratio"]
+    shape = tuple(case["shape"])
+    assert metrics.compression_ratio(32, s, shape) == closed
+    c0 = compressed(bz, case, 0)
+    assert len(bz.serialize(c0)) == nbytes
+    assert metrics.measured_ratio(32, shape, nbytes) == measured
