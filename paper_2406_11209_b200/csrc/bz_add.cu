@@ -3,6 +3,7 @@
 // both operands with the reference's exact f64 op order, block maximum,
 // rebinning -- bit-exact with the reference.
 #include "bz_common.cuh"
+#include "bz_fast.cuh"
 #include "bz_kernels.cuh"
 
 #include <type_traits>
@@ -302,6 +303,103 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
   }
 }
 
+// --------------------------------------- staged add (unaligned blocks) --
+// Blocks whose kept indices are not whole 16-byte vectors (e.g. C5's 66 int8
+// indices) are moved as contiguous tiles of TB blocks through shared memory
+// with 16-byte accesses (tile_to_smem / smem_to_tile); GS = 256/TB lanes per
+// block then read their coefficients from shared memory.  Same exact
+// arithmetic as k_add (codec.py:337-350, ops.py:178-204): the coefficient is
+// recomputed in the binning pass instead of being kept in registers.
+template <typename IT, int FK, int MODE>
+__global__ void __launch_bounds__(256)
+k_add_staged(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
+             const IT* __restrict__ a_idx, const void* __restrict__ b_max,
+             const IT* __restrict__ b_idx, int subtract, double shift,
+             void* __restrict__ out_max, IT* __restrict__ out_idx) {
+  constexpr int IK = sizeof(IT) == 1 ? BZ_I8 : BZ_I16;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const double r = radius_f64(IK), rinv = 1.0 / r;
+  const int64_t tile_bytes = (int64_t)tb * kept * sizeof(IT);
+  const int64_t region = (tile_bytes + 32 + 15) / 16 * 16;
+  unsigned char* sa = smem_raw;
+  unsigned char* sb = sa + region;
+  unsigned char* so = sb + region;
+  const int t = threadIdx.x;
+  const int gs = 256 / tb;
+  const int lb = t / gs, sub = t % gs;
+  const unsigned gmask = gs == 32 ? 0xffffffffu : (((1u << gs) - 1) << ((t & 31) - sub));
+  const int64_t ntiles = (nblocks + tb - 1) / tb;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b0 = tile * tb;
+    const int nv = (int)min((int64_t)tb, nblocks - b0);
+    const int64_t byte0 = b0 * (int64_t)kept * sizeof(IT);
+    const int64_t nbytes = (int64_t)nv * kept * sizeof(IT);
+    const int misa = (int)(((uintptr_t)a_idx + byte0) & 15);
+    const int misb = (int)(((uintptr_t)b_idx + byte0) & 15);
+    const int miso = (int)(((uintptr_t)out_idx + byte0) & 15);
+    tile_to_smem(sa, reinterpret_cast<const unsigned char*>(a_idx) + byte0, nbytes, misa, t, 256);
+    if (MODE == 0) tile_to_smem(sb, reinterpret_cast<const unsigned char*>(b_idx) + byte0, nbytes, misb, t, 256);
+    const bool valid = lb < nv;
+    const int64_t b = b0 + lb;
+    const double na = valid ? load_kind<FK>(a_max, b) : 1.0;
+    const double nb = (valid && MODE == 0) ? load_kind<FK>(b_max, b) : 1.0;
+    __syncthreads();
+    const IT* pa = reinterpret_cast<const IT*>(sa + misa) + (int64_t)lb * kept;
+    const IT* pb = reinterpret_cast<const IT*>(sb + misb) + (int64_t)lb * kept;
+    IT* po = reinterpret_cast<IT*>(so + miso) + (int64_t)lb * kept;
+    const Scale sca = make_scale(na, FK), scb = make_scale(nb, FK);
+    const bool safe = na >= 0x1p-900 && na <= 0x1p+900 &&
+                      (MODE != 0 || (nb >= 0x1p-900 && nb <= 0x1p+900));
+    auto coeff = [&](int k) -> double {
+      const int fa = (int)pa[k];
+      if (safe) {
+        const double xa = div_const(fn_product(fa, sca), r, rinv);
+        if (MODE == 0) {
+          const int fb = subtract ? -(int)pb[k] : (int)pb[k];
+          return __dadd_rn(xa, div_const(fn_product(fb, scb), r, rinv));
+        }
+        return k == 0 ? __dadd_rn(xa, shift) : xa;
+      }
+      const double xa = __ddiv_rn(__dmul_rn((double)fa, na), r);
+      if (MODE == 0) {
+        const double fb = subtract ? -(double)pb[k] : (double)pb[k];
+        return __dadd_rn(xa, __ddiv_rn(__dmul_rn(fb, nb), r));
+      }
+      return k == 0 ? __dadd_rn(xa, shift) : xa;
+    };
+    // pass 1: block maximum (NaN-propagating by bit order)
+    unsigned long long key = 0;
+    if (valid)
+#pragma unroll 4
+      for (int k = sub; k < kept; k += gs) {
+        const unsigned long long k2 = (unsigned long long)__double_as_longlong(coeff(k)) & 0x7fffffffffffffffull;
+        key = k2 > key ? k2 : key;
+      }
+    for (int o = gs / 2; o > 0; o >>= 1) {
+      const unsigned long long k2 = __shfl_xor_sync(gmask, key, o, gs);
+      key = k2 > key ? k2 : key;
+    }
+    const double mx = __longlong_as_double((long long)key);
+    const double n = round_to_kind<FK>(mx);
+    const BinCtx bc = bin_ctx(n, r, mx);
+    // pass 2: bin into the output tile (the coefficient is recomputed)
+    if (valid) {
+      if (sub == 0) store_kind<FK>(out_max, b, n);
+#pragma unroll 4
+      for (int k = sub; k < kept; k += gs) {
+        const double c = coeff(k);
+        unsigned nr = 0;
+        int q = fast_index32<IT, true>(c, bc.R, (int)r, nr);
+        if (nr | !bc.fast) q = (int)bin_exact_ctx(c, bc, r, r);
+        po[k] = (IT)q;
+      }
+    }
+    __syncthreads();
+    smem_to_tile(reinterpret_cast<unsigned char*>(out_idx) + byte0, so, nbytes, miso, t, 256);
+    __syncthreads();  // tiles reused
+  }
+}
+
 template <typename IT>
 static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                         const void* b_max, const void* b_idx, int subtract, double shift,
@@ -324,6 +422,32 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
   const int64_t threads = ga.nblocks * GS;
   const int grid = grid_for(threads, 256, 3);  // persistent: 3 CTAs per SM
   const bool same_fk = ga.float_kind == gb.float_kind || mode != 0;
+  // unaligned blocks of I8 / I16 indices: shared-memory staged tiles
+  if constexpr (sizeof(IT) <= 2) {
+    const int64_t bpb = (int64_t)kept * sizeof(IT);
+    if ((bpb % 16) != 0 && kept >= 8 && bpb <= 2048 && same_fk &&
+        (ga.float_kind == BZ_F32 || ga.float_kind == BZ_F64)) {
+      int tb = 256;  // blocks per tile: about 8 KB of indices per operand
+      while (tb > 8 && (int64_t)tb * bpb > 8192) tb >>= 1;
+      const size_t region = (size_t)((tb * bpb + 32 + 15) / 16 * 16);
+      const size_t smem = 3 * region;
+      const int64_t ntiles = (ga.nblocks + tb - 1) / tb;
+#define BZ_ST(F, M)                                                                                 \
+  {                                                                                                 \
+    auto kern = k_add_staged<IT, F, M>;                                                             \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
+    int occ = 1;                                                                                    \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);                           \
+    const int g2 = (int)std::min<int64_t>(ntiles, (int64_t)kSMs * std::max(occ, 1));                \
+    kern<<<g2, 256, smem, s>>>(ga.nblocks, kept, tb, a_max, (const IT*)a_idx, b_max,                \
+                               (const IT*)b_idx, subtract, shift, out_max, (IT*)out_idx);           \
+    return check_launch("add_staged");                                                              \
+  }
+      if (ga.float_kind == BZ_F64) { if (mode == 0) BZ_ST(BZ_F64, 0) else BZ_ST(BZ_F64, 1) }
+      else { if (mode == 0) BZ_ST(BZ_F32, 0) else BZ_ST(BZ_F32, 1) }
+#undef BZ_ST
+    }
+  }
 #define BZ_K(G, N, V, F, M)                                                                    \
   k_add<IT, G, N, V, F, M><<<grid, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind, gb.float_kind, \
                                                ga.float_kind, a_max, (const IT*)a_idx, b_max,  \
