@@ -340,8 +340,7 @@ bool fast_supported(const Geo& g, int x_kind) {
 int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s) {
   int E;
   uniform_block(g, E);
-  if (g.ndim == 3 && getenv("BZC_B200_LINE3")) return launch_line3_compress(g, x, maxima, indices, s);
-  if (g.ndim == 3 && E == 8 && !getenv("BZC_B200_SLICE3"))
+  if (g.ndim == 3 && E == 8)
     return launch_half3_compress(g, x, maxima, indices, s);
 #define BZ_CASE(DD, EE) \
   if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, x, maxima, indices, s);

@@ -323,9 +323,7 @@ bool fast_decompress_supported(const Geo& g, int out_kind) {
 int launch_fast_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s) {
   const int E = g.block[0];
-  if (g.ndim == 3 && getenv("BZC_B200_LINE3"))
-    return launch_line3_decompress(g, maxima, indices, out, out_kind, s);
-  if (g.ndim == 3 && E == 8 && !getenv("BZC_B200_SLICE3"))
+  if (g.ndim == 3 && E == 8)
     return launch_half3_decompress(g, maxima, indices, out, out_kind, s);
 #define BZ_CASE(DD, EE) \
   if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, maxima, indices, out, out_kind, s);

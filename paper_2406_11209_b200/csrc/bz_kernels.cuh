@@ -38,10 +38,6 @@ bool fast_decompress_supported(const Geo& g, int out_kind);
 int launch_half3_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s);
 int launch_half3_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                             int out_kind, cudaStream_t s);
-// 3-D blocks, one transform line per thread (bz_line3.cu)
-int launch_line3_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s);
-int launch_line3_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
-                            int out_kind, cudaStream_t s);
 int launch_fast_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s);
 
