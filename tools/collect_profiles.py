@@ -26,13 +26,13 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from ncu_summary import summarise  # noqa: E402
 
 OP_KERNELS = {  # bench op -> kernel name prefix
-    "compress": ("k_dct8_compress", "k_fast_compress", "k_half3_compress",
+    "compress": ("k_dct8_compress", "k_dct4_compress", "k_fast_compress", "k_half3_compress",
                  "k_exact_compress"),
-    "decompress": ("k_dct8_decompress", "k_fast_decompress", "k_half3_decompress",
+    "decompress": ("k_dct8_decompress", "k_dct4_decompress", "k_fast_decompress", "k_half3_decompress",
                    "k_exact_decompress"),
     "l2_norm": ("k_moments_stream", "k_moments_staged"),  # PAIR = false instantiation
     "dot": ("k_moments_stream", "k_moments_staged"),      # PAIR = true
-    "add": ("k_add",),
+    "add": ("k_add", "k_add_staged"),
 }
 
 STALL_KEYS = [
