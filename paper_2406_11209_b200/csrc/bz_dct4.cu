@@ -292,36 +292,58 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
   const int K = f.kept;
   const Dct4K KC = dct4_consts(p.H);
   const int k0 = o >> 2, k3 = o & 3;
-  // staging slot of each of this lane's 16 coefficients; dropped ones read
-  // the zero slot BS (zeroed once, never written)
+  // the warp tile's 2K indices are staged contiguously (block bs at offset
+  // bs*K); staging slot of each of this lane's 16 coefficients, dropped ones
+  // read the zero slot ZS (zeroed once, never written)
+  constexpr int ZS = 2 * BS;
   int16_t rk[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     const int r_ = f.full_mask ? (k0 * 64 + q * 4 + k3) : f.rank[k0 * 64 + q * 4 + k3];
-    rk[q] = (int16_t)(r_ >= 0 ? r_ : BS);
+    rk[q] = (int16_t)(r_ >= 0 ? r_ : ZS - bs * K);
   }
-  if (lane < 2) stg[lane * SS + BS] = (IT)0;
+  if (lane == 0) stg[ZS] = (IT)0;
   const int i1 = o >> 2, i2 = o & 3;
   double* wbase = blk + xoff(k0, 0, 0, k3);
   double* rbase = blk + xoff(0, i1, i2, 0);
-  const IT* sbase = stg + bs * SS;
-  const double rr = radius_f64(sizeof(IT) == 1 ? BZ_I8 : (sizeof(IT) == 2 ? BZ_I16 : BZ_I32));
-  const double rinv = 1.0 / rr;
+  const IT* sbase = stg + bs * K;
   const int64_t s0 = f.stride[0], s1 = f.stride[1], s2 = f.stride[2];
   const int64_t nwt = (f.nblocks + BPW - 1) / BPW;
-
-  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += (int64_t)gridDim.x * WPC) {
+  // 32-bit word copies when every warp tile starts 4-byte aligned; the next
+  // tile's words are loaded (registers) while this tile computes
+  const int64_t tile_bytes = (int64_t)BPW * K * sizeof(IT);
+  const bool words = ((uintptr_t)indices % 4 == 0) && (tile_bytes % 4 == 0) && tile_bytes <= 4 * 64;
+  uint32_t* stg32 = reinterpret_cast<uint32_t*>(stg);
+  auto load_words = [&](int64_t wt_, uint32_t& w0, uint32_t& w1) {
+    w0 = w1 = 0u;
+    if (wt_ < nwt) {
+      const int64_t b0 = wt_ * BPW;
+      const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
+      const int nw = (int)((nv * K * (int64_t)sizeof(IT) + 3) / 4);
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(indices + b0 * (int64_t)K);
+      if (lane < nw) w0 = __ldcs(src + lane);
+      if (lane + 32 < nw) w1 = __ldcs(src + lane + 32);
+    }
+  };
+  uint32_t nw0 = 0, nw1 = 0;
+  const int64_t wstride = (int64_t)gridDim.x * WPC;
+  const double rr = radius_f64(sizeof(IT) == 1 ? BZ_I8 : (sizeof(IT) == 2 ? BZ_I16 : BZ_I32));
+  const double rinv = 1.0 / rr;
+  if (words) load_words(blockIdx.x * (int64_t)WPC + w, nw0, nw1);
+  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += wstride) {
     const int64_t b = wt * BPW + bs;
     const bool valid = b < f.nblocks;
-    // ---- the warp tile's kept indices -> staging (element granularity)
-    {
+    // ---- the warp tile's kept indices -> staging
+    if (words) {
+      const int nw = (int)((min((int64_t)BPW, f.nblocks - wt * BPW) * K * (int64_t)sizeof(IT) + 3) / 4);
+      if (lane < nw) stg32[lane] = nw0;
+      if (lane + 32 < nw) stg32[lane + 32] = nw1;
+      load_words(wt + wstride, nw0, nw1);
+    } else {
       const int64_t b0 = wt * BPW;
       const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
       const IT* src = indices + b0 * (int64_t)K;
-      for (int e = lane; e < nv * K; e += 32) {
-        const int blk_i = e >= K, off = e - blk_i * K;
-        stg[blk_i * SS + off] = __ldcs(src + e);
-      }
+      for (int e = lane; e < nv * K; e += 32) stg[e] = __ldcs(src + e);
     }
     const double nmax = valid ? load_kind<FK>(maxima, b) : 0.0;
     const bool odd = !(nmax >= 0x1p-900 && nmax <= 0x1p+1000);
