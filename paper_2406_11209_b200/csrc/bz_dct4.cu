@@ -107,18 +107,20 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
   const int K = f.kept;
   const Dct4K KC = dct4_consts(p.H);
   // this lane's 16 output positions (k0 = o>>2, k3 = o&3, k1, k2) -> staging
-  // slot (rank; dropped coefficients go to the scratch slot BS)
+  // slot: the warp tile's 2K indices are staged contiguously (block bs at
+  // bs*K); dropped coefficients go to the scratch slot ZS
+  constexpr int ZS = 2 * BS;
   const int k0 = o >> 2, k3 = o & 3;
   int16_t rk[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     const int r_ = f.full_mask ? (k0 * 64 + q * 4 + k3) : f.rank[k0 * 64 + q * 4 + k3];
-    rk[q] = (int16_t)(r_ >= 0 ? r_ : BS);
+    rk[q] = (int16_t)(r_ >= 0 ? r_ : ZS - bs * K);
   }
   const int i1 = o >> 2, i2 = o & 3;
   double* wbase = blk + xoff(0, i1, i2, 0);  // phase A: (a0, a3) at immediates
   double* rbase = blk + xoff(k0, 0, 0, k3);  // phase B: (a1, a2) at immediates
-  int8_t* sbase = stg + bs * SS;
+  int8_t* sbase = stg + bs * K;
   const int64_t s0 = f.stride[0], s1 = f.stride[1], s2 = f.stride[2];
   const int64_t nwt = (f.nblocks + BPW - 1) / BPW;
 
@@ -230,7 +232,7 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
     for (int q = 0; q < 16; ++q) {
       const int fx = __double2loint(__fma_rn(v[q], R16, 1.5 * 268435456.0));
       const unsigned y1 = (unsigned)fx + (1u << 23) + 1u;
-      zmin = min(zmin, rk[q] < BS ? (y1 & 0xffffffu) : 0xffffffffu);  // kept coefficients only
+      zmin = min(zmin, rk[q] != ZS - bs * K ? (y1 & 0xffffffu) : 0xffffffffu);  // kept only
       sbase[rk[q]] = (int8_t)(y1 >> 24);
     }
     bad = bad || zmin <= 2u;
@@ -246,30 +248,13 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
       const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
       const int nbytes = nv * K;
       int8_t* dst = indices + b0 * (int64_t)K;
-      // the two staged blocks sit at stg[0..K) and stg[SS..SS+K)
-      if (((uintptr_t)dst & 3) == 0 && (K & 3) == 0) {
-        for (int i = lane; i < nbytes / 4; i += 32) {
-          const int e = i * 4;
-          const int blk_i = e / K, off = e - blk_i * K;
-          reinterpret_cast<uint32_t*>(dst)[i] = *reinterpret_cast<const uint32_t*>(stg + blk_i * SS + off);
-        }
-      } else if (((uintptr_t)dst & 3) == 0 && ((2 * K) & 3) == 0 && nv == BPW) {
-        // K = 2 mod 4 (e.g. 66): assemble words across the block seam
-        for (int i = lane; i < nbytes / 4; i += 32) {
-          uint32_t wd = 0;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int e = i * 4 + j;
-            const int blk_i = e >= K, off = e - blk_i * K;
-            wd |= (uint32_t)(uint8_t)stg[blk_i * SS + off] << (8 * j);
-          }
-          reinterpret_cast<uint32_t*>(dst)[i] = wd;
-        }
+      // staged contiguously: one word per lane (and a second) when aligned
+      if ((((uintptr_t)dst | (uintptr_t)nbytes) & 3) == 0) {
+        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+        for (int i = lane; i < nbytes / 4; i += 32) __stcs(d32 + i, s32[i]);
       } else {
-        for (int e = lane; e < nbytes; e += 32) {
-          const int blk_i = e >= K, off = e - blk_i * K;
-          dst[e] = stg[blk_i * SS + off];
-        }
+        for (int e2 = lane; e2 < nbytes; e2 += 32) dst[e2] = stg[e2];
       }
     }
     __syncwarp();  // staging and exchange area reused by the next tile
