@@ -93,7 +93,8 @@ def main():
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
     traffic_path = os.path.join(prof, "ncu_traffic.json")
-    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    old = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    traffic = {}  # rebuilt from this round's launch lists; workloads not profiled keep old values
 
     for path in sorted(glob.glob(os.path.join(args.src, "launches_*.csv"))):
         w = os.path.basename(path)[len("launches_"):-4]
@@ -122,7 +123,7 @@ def main():
                 if any(name.split("<")[0].endswith(p) or name.startswith("void " + p) or name.startswith(p)
                        for p in prefixes) and dram:
                     key = f"{w}:{op}"
-                    if "to_kind" not in key:
+                    if "to_kind" not in key and key not in traffic:  # dominant kernel first
                         traffic[key] = statistics.median(dram)
         with open(os.path.join(prof, f"{tag}_launches_{w}.txt"), "w") as fh:
             fh.write("\n".join(lines) + "\n")
@@ -146,6 +147,8 @@ def main():
             w = "c2" if "C2" in d.get("config", {}).get("workload", "") else "x"
             with open(os.path.join(prof, f"{tag}_bench_{w}.json"), "w") as fh:
                 json.dump(d, fh, indent=1)
+    for k, v in old.items():
+        traffic.setdefault(k, v)
     with open(traffic_path, "w") as fh:
         json.dump(traffic, fh, indent=1, sort_keys=True)
 
