@@ -70,6 +70,20 @@ __device__ __forceinline__ double fn_product(long long f, const Scale& s) {
   return __dmul_rn((double)f, s.n);
 }
 
+// element e of a 16-byte chunk (compile-time e)
+template <typename IT>
+__device__ __forceinline__ elem_t<IT> vec_elem(const uint4& w, int e) {
+  const uint32_t x = (e * (int)sizeof(IT)) / 4 == 0 ? w.x : (e * (int)sizeof(IT)) / 4 == 1 ? w.y
+                   : (e * (int)sizeof(IT)) / 4 == 2 ? w.z : w.w;
+  if constexpr (sizeof(IT) == 1) return (int8_t)(x >> (8 * (e % 4)));
+  else if constexpr (sizeof(IT) == 2) return (int16_t)(x >> (16 * (e % 2)));
+  else if constexpr (sizeof(IT) == 4) return (int32_t)x;
+  else {
+    const uint32_t hi = (e * 8) / 4 + 1 == 1 ? w.y : w.w;
+    return (long long)(((unsigned long long)hi << 32) | x);
+  }
+}
+
 // one chunk (16 bytes) of a block's kept indices as integers
 template <typename IT>
 __device__ __forceinline__ void unpack_chunk(const uint4& w, elem_t<IT> (&out)[16 / sizeof(IT)]) {
@@ -169,44 +183,52 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
                       (mode != 0 || (nb >= 0x1p-900 && nb <= 0x1p+900));
     double c[L];
     unsigned long long key = 0;
+    // block-uniform choice of the arithmetic: the common (safe) path has no
+    // per-coefficient branch; unsafe maxima (tiny / huge) use IEEE division
+    auto coeffs = [&](auto safe_tag) {
+      constexpr bool SAFE = decltype(safe_tag)::value;
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) {
-      const int k0 = (ch * GS + sub) * V;
-      elem_t<IT> fa[V], fb[V];
-      if (VEC) {
-        unpack_chunk<IT>(ca[ch], fa);
-        unpack_chunk<IT>(cb[ch], fb);
-      } else {
-        load_chunk<IT>(a_idx, base, k0, kept, false, fa);
-        if (mode == 0) load_chunk<IT>(b_idx, base, k0, kept, false, fb);
-      }
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int k0 = (ch * GS + sub) * V;
+        elem_t<IT> fa[V], fb[V];
+        if (!VEC) {
+          load_chunk<IT>(a_idx, base, k0, kept, false, fa);
+          if (mode == 0) load_chunk<IT>(b_idx, base, k0, kept, false, fb);
+        }
 #pragma unroll
-      for (int e = 0; e < V; ++e) {
-        double cc;
-        if (safe) {
-          const double xa = div_const(fn_product(fa[e], sa), r, rinv);
-          if (mode == 0) {
-            const elem_t<IT> fbv = subtract ? -fb[e] : fb[e];
-            cc = __dadd_rn(xa, div_const(fn_product(fbv, sb), r, rinv));
-          } else {
-            cc = (k0 + e == 0) ? __dadd_rn(xa, shift) : xa;
+        for (int e = 0; e < V; ++e) {
+          if (VEC) {  // extract on the fly (no unpacked copies held in registers)
+            fa[e] = vec_elem<IT>(ca[ch], e);
+            fb[e] = vec_elem<IT>(cb[ch], e);
           }
-        } else {
-          const double xa = spec_coeff_slow((double)fa[e], na, r);
-          if (mode == 0) {
-            const double fbv = subtract ? -(double)fb[e] : (double)fb[e];
-            cc = __dadd_rn(xa, spec_coeff_slow(fbv, nb, r));
+          double cc;
+          if constexpr (SAFE) {
+            const double xa = div_const(fn_product(fa[e], sa), r, rinv);
+            if (mode == 0) {
+              const elem_t<IT> fbv = subtract ? -fb[e] : fb[e];
+              cc = __dadd_rn(xa, div_const(fn_product(fbv, sb), r, rinv));
+            } else {
+              cc = (k0 + e == 0) ? __dadd_rn(xa, shift) : xa;
+            }
           } else {
-            cc = (k0 + e == 0) ? __dadd_rn(xa, shift) : xa;
+            const double xa = spec_coeff_slow((double)fa[e], na, r);
+            if (mode == 0) {
+              const double fbv = subtract ? -(double)fb[e] : (double)fb[e];
+              cc = __dadd_rn(xa, spec_coeff_slow(fbv, nb, r));
+            } else {
+              cc = (k0 + e == 0) ? __dadd_rn(xa, shift) : xa;
+            }
+          }
+          c[ch * V + e] = cc;
+          if (VEC ? (k0 < kept) : (k0 + e < kept)) {  // VEC: chunks are whole
+            const unsigned long long k2 = (unsigned long long)__double_as_longlong(cc) & 0x7fffffffffffffffull;
+            key = k2 > key ? k2 : key;
           }
         }
-        c[ch * V + e] = cc;
-        if (VEC ? (k0 < kept) : (k0 + e < kept)) {  // VEC: chunks are whole
-          const unsigned long long k2 = (unsigned long long)__double_as_longlong(cc) & 0x7fffffffffffffffull;
-          key = k2 > key ? k2 : key;
-        }
       }
-    }
+    };
+    if (safe) coeffs(std::true_type{});
+    else coeffs(std::false_type{});
 #pragma unroll
     for (int o = GS / 2; o > 0; o >>= 1) {
       const unsigned long long k2 = __shfl_xor_sync(gmask, key, o, GS);
