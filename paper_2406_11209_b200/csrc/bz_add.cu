@@ -183,6 +183,7 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
                       (mode != 0 || (nb >= 0x1p-900 && nb <= 0x1p+900));
     double c[L];
     unsigned long long key = 0;
+    double mxd = 0.0;
     // block-uniform choice of the arithmetic: the common (safe) path has no
     // per-coefficient branch; unsafe maxima (tiny / huge) use IEEE division
     auto coeffs = [&](auto safe_tag) {
@@ -221,11 +222,17 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
           }
           c[ch * V + e] = cc;
           if (VEC ? (k0 < kept) : (k0 + e < kept)) {  // VEC: chunks are whole
-            const unsigned long long k2 = (unsigned long long)__double_as_longlong(cc) & 0x7fffffffffffffffull;
-            key = k2 > key ? k2 : key;
+            if constexpr (SAFE) {  // finite on the safe path: plain compare-select
+              const double a = fabs(cc);
+              mxd = a > mxd ? a : mxd;
+            } else {  // NaN-propagating via the bit order
+              const unsigned long long k2 = (unsigned long long)__double_as_longlong(cc) & 0x7fffffffffffffffull;
+              key = k2 > key ? k2 : key;
+            }
           }
         }
       }
+      if constexpr (SAFE) key = (unsigned long long)__double_as_longlong(mxd);
     };
     if (safe) coeffs(std::true_type{});
     else coeffs(std::false_type{});
@@ -422,6 +429,126 @@ k_add_staged(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
   }
 }
 
+// Register-cached variant of the staged add: GS lanes per block (compile
+// time), each lane keeps its CPL coefficients in registers so they are
+// computed once; a tile of TB blocks' indices AND maxima is staged in shared
+// memory, and the groups of the CTA walk the tile's blocks.
+template <typename IT, int FK, int MODE, int GS, int CPL>
+__global__ void __launch_bounds__(256, 3)
+k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
+            const IT* __restrict__ a_idx, const void* __restrict__ b_max,
+            const IT* __restrict__ b_idx, int subtract, double shift,
+            void* __restrict__ out_max, IT* __restrict__ out_idx) {
+  constexpr int IK = sizeof(IT) == 1 ? BZ_I8 : BZ_I16;
+  using MT = typename std::conditional<FK == BZ_F64, double, float>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const double r = radius_f64(IK), rinv = 1.0 / r;
+  const int64_t region = ((int64_t)tb * kept * sizeof(IT) + 32 + 15) / 16 * 16;
+  unsigned char* sa = smem_raw;
+  unsigned char* sb = sa + region;
+  unsigned char* so = sb + region;
+  MT* sma = reinterpret_cast<MT*>(so + region);
+  MT* smb = sma + tb;
+  const int t = threadIdx.x;
+  const int lane = t & 31;
+  const int sub = lane % GS;
+  const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1) << (lane - sub));
+  const int64_t ntiles = (nblocks + tb - 1) / tb;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b0 = tile * tb;
+    const int nv = (int)min((int64_t)tb, nblocks - b0);
+    const int64_t byte0 = b0 * (int64_t)kept * sizeof(IT);
+    const int64_t nbytes = (int64_t)nv * kept * sizeof(IT);
+    const int misa = (int)(((uintptr_t)a_idx + byte0) & 15);
+    const int misb = (int)(((uintptr_t)b_idx + byte0) & 15);
+    const int miso = (int)(((uintptr_t)out_idx + byte0) & 15);
+    for (int i = t; i < nv; i += 256) {
+      sma[i] = reinterpret_cast<const MT*>(a_max)[b0 + i];
+      if (MODE == 0) smb[i] = reinterpret_cast<const MT*>(b_max)[b0 + i];
+    }
+    tile_to_smem(sa, reinterpret_cast<const unsigned char*>(a_idx) + byte0, nbytes, misa, t, 256);
+    if (MODE == 0) tile_to_smem(sb, reinterpret_cast<const unsigned char*>(b_idx) + byte0, nbytes, misb, t, 256);
+    __syncthreads();
+    for (int lb = t / GS; lb < nv; lb += 256 / GS) {
+      const int64_t b = b0 + lb;
+      const IT* pa = reinterpret_cast<const IT*>(sa + misa) + (int64_t)lb * kept;
+      const IT* pb = reinterpret_cast<const IT*>(sb + misb) + (int64_t)lb * kept;
+      IT* po = reinterpret_cast<IT*>(so + miso) + (int64_t)lb * kept;
+      const double na = (double)sma[lb];
+      const double nb = MODE == 0 ? (double)smb[lb] : 1.0;
+      const Scale sca = make_scale(na, FK), scb = make_scale(nb, FK);
+      const bool safe = na >= 0x1p-900 && na <= 0x1p+900 &&
+                        (MODE != 0 || (nb >= 0x1p-900 && nb <= 0x1p+900));
+      double c[CPL];
+      unsigned long long key = 0;
+      auto coeffs = [&](auto safe_tag) {
+        constexpr bool SAFE = decltype(safe_tag)::value;
+        double mxd = 0.0;
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+          const int k = sub + j * GS;
+          double cc = 0.0;
+          if (k < kept) {
+            const int fa = (int)pa[k];
+            if constexpr (SAFE) {
+              const double xa = div_const(fn_product(fa, sca), r, rinv);
+              if (MODE == 0) {
+                const int fb = subtract ? -(int)pb[k] : (int)pb[k];
+                cc = __dadd_rn(xa, div_const(fn_product(fb, scb), r, rinv));
+              } else {
+                cc = k == 0 ? __dadd_rn(xa, shift) : xa;
+              }
+              const double a = fabs(cc);
+              mxd = a > mxd ? a : mxd;
+            } else {
+              const double xa = spec_coeff_slow((double)fa, na, r);
+              if (MODE == 0) {
+                const double fb = subtract ? -(double)pb[k] : (double)pb[k];
+                cc = __dadd_rn(xa, spec_coeff_slow(fb, nb, r));
+              } else {
+                cc = k == 0 ? __dadd_rn(xa, shift) : xa;
+              }
+              const unsigned long long k2 = (unsigned long long)__double_as_longlong(cc) & 0x7fffffffffffffffull;
+              key = k2 > key ? k2 : key;
+            }
+          }
+          c[j] = cc;
+        }
+        if constexpr (SAFE) key = (unsigned long long)__double_as_longlong(mxd);
+      };
+      if (safe) coeffs(std::true_type{});
+      else coeffs(std::false_type{});
+#pragma unroll
+      for (int o = GS / 2; o > 0; o >>= 1) {
+        const unsigned long long k2 = __shfl_xor_sync(gmask, key, o, GS);
+        key = k2 > key ? k2 : key;
+      }
+      const double mx = __longlong_as_double((long long)key);
+      const double n = round_to_kind<FK>(mx);
+      const BinCtx bc = bin_ctx(n, r, mx);
+      if (sub == 0) store_kind<FK>(out_max, b, n);
+      int q[CPL];
+      unsigned nacc = 0;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) q[j] = fast_index32<IT, true>(c[j], bc.R, (int)r, nacc);
+      if (nacc | !bc.fast) {
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+          unsigned nr = 0;
+          fast_index32<IT, true>(c[j], bc.R, (int)r, nr);
+          if (nr | !bc.fast) q[j] = (int)bin_exact_ctx(c[j], bc, r, r);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CPL; ++j)
+        if (sub + j * GS < kept) po[sub + j * GS] = (IT)q[j];
+    }
+    __syncthreads();
+    smem_to_tile(reinterpret_cast<unsigned char*>(out_idx) + byte0, so, nbytes, miso, t, 256);
+    __syncthreads();  // tiles reused
+  }
+}
+
 template <typename IT>
 static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                         const void* b_max, const void* b_idx, int subtract, double shift,
@@ -449,6 +576,38 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
     const int64_t bpb = (int64_t)kept * sizeof(IT);
     if ((bpb % 16) != 0 && kept >= 8 && bpb <= 2048 && same_fk &&
         (ga.float_kind == BZ_F32 || ga.float_kind == BZ_F64)) {
+      if (kept <= 512) {  // register-cached tiles
+        const int gs = kept <= 128 ? 8 : 32;
+        const int cpl = (kept + gs - 1) / gs;
+        const int tbt = std::max(256 / gs, (int)(8192 / bpb) / (256 / gs) * (256 / gs));
+        const size_t region = (size_t)((tbt * bpb + 32 + 15) / 16 * 16);
+        const size_t smem = 3 * region + 2 * (size_t)tbt * (ga.float_kind == BZ_F64 ? 8 : 4);
+        const int64_t ntiles = (ga.nblocks + tbt - 1) / tbt;
+#define BZ_TT(F, M, G, C)                                                                           \
+  {                                                                                                 \
+    auto kern = k_add_tiled<IT, F, M, G, C>;                                                        \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
+    int occ = 1;                                                                                    \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);                           \
+    const int g2 = (int)std::min<int64_t>(ntiles, (int64_t)kSMs * std::max(occ, 1));                \
+    kern<<<g2, 256, smem, s>>>(ga.nblocks, kept, tbt, a_max, (const IT*)a_idx, b_max,               \
+                               (const IT*)b_idx, subtract, shift, out_max, (IT*)out_idx);           \
+    return check_launch("add_tiled");                                                               \
+  }
+#define BZ_TC(F, M)                                                     \
+  {                                                                     \
+    if (gs == 8) {                                                      \
+      if (cpl <= 4) BZ_TT(F, M, 8, 4) else if (cpl <= 8) BZ_TT(F, M, 8, 8) \
+      else if (cpl <= 12) BZ_TT(F, M, 8, 12) else BZ_TT(F, M, 8, 16)      \
+    } else {                                                            \
+      if (cpl <= 8) BZ_TT(F, M, 32, 8) else BZ_TT(F, M, 32, 16)         \
+    }                                                                   \
+  }
+        if (ga.float_kind == BZ_F64) { if (mode == 0) BZ_TC(BZ_F64, 0) else BZ_TC(BZ_F64, 1) }
+        else { if (mode == 0) BZ_TC(BZ_F32, 0) else BZ_TC(BZ_F32, 1) }
+#undef BZ_TC
+#undef BZ_TT
+      }
       int tb = 256;  // blocks per tile: about 8 KB of indices per operand
       while (tb > 8 && (int64_t)tb * bpb > 8192) tb >>= 1;
       const size_t region = (size_t)((tb * bpb + 32 + 15) / 16 * 16);

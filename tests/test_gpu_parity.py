@@ -376,3 +376,41 @@ def test_dct4_flagged_blocks(bz, monkeypatch, mask):
     fin = np.isfinite(ref)
     assert np.array_equal(np.isnan(dec), np.isnan(ref))
     assert np.all(np.abs(dec[fin] - ref[fin]) <= 1e-13 * np.max(np.abs(ref[fin])))
+
+
+@pytest.mark.parametrize("block,fk,ik,keep", [
+    ((8, 8), "f32", "i8", 9),            # tiled add: 8 lanes per block, 4 per lane
+    ((8, 8), "f64", "i16", 37),          # 74-byte blocks
+    ((16, 16), "f32", "i8", 100),        # 8 lanes x 16
+    ((16, 16), "f64", "i8", 200),        # 32 lanes per block
+    ((8, 8, 16), "f32", "i16", 300),     # 32 lanes x 16 (600-byte blocks)
+    ((8, 8, 16), "f64", "i8", 700),      # > 512 kept: two-pass staged add
+])
+def test_elementwise_unaligned_blocks(bz, block, fk, ik, keep):
+    """add / subtract / add_scalar / negate on blocks whose kept indices are
+    not whole 16-byte vectors (the shared-memory tiled kernels), including
+    zero, NaN, tiny and huge blocks; bit-exact with the oracle."""
+    rng = np.random.default_rng(keep)
+    grid = (5, 3) + (1,) * (len(block) - 2)
+    shape = tuple(b * g for b, g in zip(block, grid))
+    bits = np.zeros(int(np.prod(block)), bool)
+    bits[0] = True
+    bits[1 + rng.permutation(bits.size - 1)[:keep - 1]] = True
+    bits = bits.reshape(block)
+    s = _settings(bz, block, fk, ik, mask_bits=bits)
+    os_ = o.Settings(block, fk, ik, "dct", bits)
+    xa = rng.normal(size=shape)
+    xb = 0.4 * xa + rng.normal(size=shape)
+    sl = lambda i: tuple([slice(i * block[0], (i + 1) * block[0])] + [slice(0, b) for b in block[1:]])
+    xa[sl(0)] = 0.0
+    xb[sl(1)] = np.nan
+    xa[sl(2)] *= 1e-300 if fk == "f64" else 1e-30
+    xb[sl(3)] *= 1e300 if fk == "f64" else 1e30
+    ra, rb = o.compress(o.round_to_kind(xa, fk), os_), o.compress(o.round_to_kind(xb, fk), os_)
+    a = bz.CompressedArray(shape, s, ra.maxima, ra.indices)
+    b = bz.CompressedArray(shape, s, rb.maxima, rb.indices)
+    for got, want in ((bz.add(a, b), o.add(ra, rb)), (bz.subtract(a, b), o.subtract(ra, rb)),
+                      (bz.add_scalar(a, 0.25), o.add_scalar(ra, 0.25)),
+                      (bz.negate(b), o.negate(rb))):
+        assert np.array_equal(got.maxima_f64().cpu().numpy(), want.maxima, equal_nan=True)
+        assert np.array_equal(got.indices.cpu().numpy(), want.indices)
