@@ -97,6 +97,32 @@ __device__ __forceinline__ void unpack_chunk(const uint4& w, elem_t<IT> (&out)[1
   }
 }
 
+// deterministic sum of every thread's red_acc into red_ws[1]: warp tree, CTA
+// tree, the last CTA sums the CTA partials in index order (red_ws layout:
+// [arrival counter, result, CTA partials]; the counter is re-armed)
+__device__ __forceinline__ void red_finish(double red_acc, double* __restrict__ red_ws) {
+  for (int o = 16; o > 0; o >>= 1) red_acc += __shfl_xor_sync(0xffffffffu, red_acc, o);
+  __shared__ double wsum[8];
+  __shared__ bool last;
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = red_acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += wsum[i];
+    red_ws[2 + blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(reinterpret_cast<unsigned int*>(red_ws), 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(red_ws + 2 + i);
+    red_ws[1] = s;
+    *reinterpret_cast<unsigned int*>(red_ws) = 0u;  // re-arm
+  }
+}
+
 // mode 0: a + (+/-)b     mode 1: a + shift at the first coefficient (add_scalar)
 // A group of GS lanes handles one block; each lane keeps NCH chunks of V
 // coefficients in registers (GS*NCH*V >= kept), so the block is read once.
@@ -307,29 +333,7 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
     }
     if (RED) red_acc = __fma_rn((double)red_sq, n * n, red_acc);
   }
-  if constexpr (RED) {
-    // deterministic: warp tree, CTA tree, last CTA sums the CTA partials in order
-    for (int o = 16; o > 0; o >>= 1) red_acc += __shfl_xor_sync(0xffffffffu, red_acc, o);
-    __shared__ double wsum[8];
-    __shared__ bool last;
-    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = red_acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += wsum[i];
-      red_ws[2 + blockIdx.x] = s;
-      __threadfence();
-      last = atomicAdd(reinterpret_cast<unsigned int*>(red_ws), 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (last && threadIdx.x == 0) {
-      __threadfence();
-      double s = 0.0;
-      for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(red_ws + 2 + i);
-      red_ws[1] = s;
-      *reinterpret_cast<unsigned int*>(red_ws) = 0u;  // re-arm
-    }
-  }
+  if constexpr (RED) red_finish(red_acc, red_ws);
 }
 
 // --------------------------------------- staged add (unaligned blocks) --
@@ -433,12 +437,16 @@ k_add_staged(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
 // time), each lane keeps its CPL coefficients in registers so they are
 // computed once; a tile of TB blocks' indices AND maxima is staged in shared
 // memory, and the groups of the CTA walk the tile's blocks.
-template <typename IT, int FK, int MODE, int GS, int CPL>
+// RED: accumulate the result's squared L2 norm instead of storing it (the
+// fused time-series step, as k_add<..., RED>).
+template <typename IT, int FK, int MODE, int GS, int CPL, bool RED = false>
 __global__ void __launch_bounds__(256, 3)
 k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
             const IT* __restrict__ a_idx, const void* __restrict__ b_max,
             const IT* __restrict__ b_idx, int subtract, double shift,
-            void* __restrict__ out_max, IT* __restrict__ out_idx) {
+            void* __restrict__ out_max, IT* __restrict__ out_idx,
+            double* __restrict__ red_ws = nullptr) {
+  double red_acc = 0.0;
   constexpr int IK = sizeof(IT) == 1 ? BZ_I8 : BZ_I16;
   using MT = typename std::conditional<FK == BZ_F64, double, float>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -526,7 +534,7 @@ k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
       const double mx = __longlong_as_double((long long)key);
       const double n = round_to_kind<FK>(mx);
       const BinCtx bc = bin_ctx(n, r, mx);
-      if (sub == 0) store_kind<FK>(out_max, b, n);
+      if (!RED && sub == 0) store_kind<FK>(out_max, b, n);
       int q[CPL];
       unsigned nacc = 0;
 #pragma unroll
@@ -539,14 +547,27 @@ k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
           if (nr | !bc.fast) q[j] = (int)bin_exact_ctx(c[j], bc, r, r);
         }
       }
+      if constexpr (RED) {
+        int sq = 0;  // exact: <= CPL * 32767^2 < 2^31 for CPL <= 2
+        long long sq64 = 0;
 #pragma unroll
-      for (int j = 0; j < CPL; ++j)
-        if (sub + j * GS < kept) po[sub + j * GS] = (IT)q[j];
+        for (int j = 0; j < CPL; ++j)
+          if (sub + j * GS < kept) {
+            if constexpr (sizeof(IT) == 1) sq += q[j] * q[j];
+            else sq64 += (long long)(q[j] * q[j]);
+          }
+        red_acc = __fma_rn((double)(sq64 + sq), n * n, red_acc);
+      } else {
+#pragma unroll
+        for (int j = 0; j < CPL; ++j)
+          if (sub + j * GS < kept) po[sub + j * GS] = (IT)q[j];
+      }
     }
     __syncthreads();
-    smem_to_tile(reinterpret_cast<unsigned char*>(out_idx) + byte0, so, nbytes, miso, t, 256);
+    if (!RED) smem_to_tile(reinterpret_cast<unsigned char*>(out_idx) + byte0, so, nbytes, miso, t, 256);
     __syncthreads();  // tiles reused
   }
+  if constexpr (RED) red_finish(red_acc, red_ws);
 }
 
 template <typename IT>
@@ -591,7 +612,7 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);                           \
     const int g2 = (int)std::min<int64_t>(ntiles, (int64_t)kSMs * std::max(occ, 1));                \
     kern<<<g2, 256, smem, s>>>(ga.nblocks, kept, tbt, a_max, (const IT*)a_idx, b_max,               \
-                               (const IT*)b_idx, subtract, shift, out_max, (IT*)out_idx);           \
+                               (const IT*)b_idx, subtract, shift, out_max, (IT*)out_idx, nullptr);  \
     return check_launch("add_tiled");                                                               \
   }
 #define BZ_TC(F, M)                                                     \
@@ -682,6 +703,43 @@ static int launch_subtract_l2_t(const Geo& ga, const Geo& gb, const void* a_max,
     NCH = NCH <= 1 ? 1 : (NCH <= 2 ? 2 : 4);
   }
   const bool vec = ((kept * sizeof(IT)) % 16 == 0) && !(((uintptr_t)a_idx | (uintptr_t)b_idx) & 15);
+  const int64_t bpb = (int64_t)kept * sizeof(IT);
+  if (!vec && kept >= 8 && kept <= 512 && bpb <= 2048 && ga.float_kind == gb.float_kind &&
+      (ga.float_kind == BZ_F32 || ga.float_kind == BZ_F64)) {
+    // unaligned blocks: register-cached shared-memory tiles (k_add_tiled)
+    const int gs = kept <= 128 ? 8 : 32;
+    const int cpl = (kept + gs - 1) / gs;
+    const int tbt = std::max(256 / gs, (int)(8192 / bpb) / (256 / gs) * (256 / gs));
+    const size_t region = (size_t)((tbt * bpb + 32 + 15) / 16 * 16);
+    const size_t smem = 3 * region + 2 * (size_t)tbt * (ga.float_kind == BZ_F64 ? 8 : 4);
+    const int64_t ntiles = (ga.nblocks + tbt - 1) / tbt;
+#define BZ_TT(F, G, C)                                                                              \
+  {                                                                                                 \
+    auto kern = k_add_tiled<IT, F, 0, G, C, true>;                                                  \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
+    int occ = 1;                                                                                    \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);                           \
+    const int g2 = (int)std::min<int64_t>(ntiles, (int64_t)kSMs * std::min(std::max(occ, 1), 3));   \
+    kern<<<g2, 256, smem, s>>>(ga.nblocks, kept, tbt, a_max, (const IT*)a_idx, b_max,               \
+                               (const IT*)b_idx, 1, 0.0, nullptr, nullptr, ws);                     \
+  }
+#define BZ_TC(F)                                                            \
+  {                                                                         \
+    if (gs == 8) {                                                          \
+      if (cpl <= 4) BZ_TT(F, 8, 4) else if (cpl <= 8) BZ_TT(F, 8, 8)        \
+      else if (cpl <= 12) BZ_TT(F, 8, 12) else BZ_TT(F, 8, 16)              \
+    } else {                                                                \
+      if (cpl <= 8) BZ_TT(F, 32, 8) else BZ_TT(F, 32, 16)                   \
+    }                                                                       \
+  }
+    if (ga.float_kind == BZ_F64) BZ_TC(BZ_F64) else BZ_TC(BZ_F32)
+#undef BZ_TC
+#undef BZ_TT
+    if (int rc = check_launch("subtract_l2_tiled")) return rc;
+    if (cudaMemcpyAsync(out, ws + 1, sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return check_launch("subtract_l2 copy");
+    return BZ_OK;
+  }
   if (!vec || ga.float_kind != gb.float_kind ||
       (ga.float_kind != BZ_F32 && ga.float_kind != BZ_F64))
     return BZ_E_UNSUPPORTED;

@@ -619,7 +619,11 @@ static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const v
                         double* record, cudaStream_t s) {
   const int64_t B = ga.nblocks;
   const int kept = ga.kept;
-  if (dc_only && kept > 0) {
+  // dc_only == 2 ("sums"): no DC moments -- every kept position, the first
+  // included, goes into S_* (the record of a mask without the first
+  // coefficient); dot / l2 need nothing else
+  const int kf = dc_only == 2 ? 0 : ga.keeps_first;
+  if (dc_only == 1 && kept > 0) {
     constexpr int U = 8;
     auto kern = k_moments_dc<IT, U, PAIR>;
     const int grid = persistent_grid(kern, 256, 0, (B + 256 * U - 1) / (256 * U));
@@ -639,7 +643,7 @@ static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const v
     constexpr int UU = NWV == 8 ? U / 2 : U;                                                     \
     auto kern = k_moments_stream<IT, NWV, UU, PAIR, FKV, SP>;                                    \
     const int grid = persistent_grid(kern, 256, 0, (chunks + 256 * UU - 1) / (256 * UU));       \
-    kern<<<grid, 256, 0, s>>>(B, kept, ga.keeps_first, ga.float_kind, gb.float_kind, a_max,      \
+    kern<<<grid, 256, 0, s>>>(B, kept, kf, ga.float_kind, gb.float_kind, a_max,                  \
                               (const IT*)a_idx, b_max, (const IT*)b_idx, ws, record);            \
     return check_launch("moments_stream");                                                       \
   }
@@ -664,7 +668,7 @@ static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const v
   auto kern = k_moments_staged<IT, PAIR>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = persistent_grid(kern, 256, smem, (B + 255) / 256);
-  kern<<<grid, 256, smem, s>>>(B, kept, ga.keeps_first, ga.float_kind, gb.float_kind, a_max,
+  kern<<<grid, 256, smem, s>>>(B, kept, kf, ga.float_kind, gb.float_kind, a_max,
                                (const IT*)a_idx, b_max, (const IT*)b_idx, ws, record);
   return check_launch("moments_staged");
 }

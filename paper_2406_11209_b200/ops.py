@@ -235,7 +235,7 @@ def _reduce_workspace(dev: torch.device, nbytes: int) -> torch.Tensor:
 
 
 def moments_record(a: CompressedArray, b: CompressedArray | None = None, *,
-                   dc_only: bool = False) -> torch.Tensor:
+                   dc_only: int = 0) -> torch.Tensor:
     """Launch the fused reduction; returns the device record (16 float64)."""
     pair = b is not None and b is not a
     dev = a.device
@@ -283,6 +283,11 @@ def record_to_host(rec: torch.Tensor) -> np.ndarray:
     return h.numpy().copy()
 
 
+# dc_only = 2: plain sums over every kept position (no DC moments) -- all that
+# dot and l2_norm need (include/bzc_b200.h, bz_moments)
+_SUMS = 2
+
+
 def _reduce(a, b=None, *, dc_only=False) -> Record:
     """Record of the whole array (sharded arrays merge across ranks first)."""
     hook = getattr(a, "_reduce_record", None)
@@ -323,16 +328,16 @@ def dot(a: CompressedArray, b: CompressedArray) -> float:
     _check_compatible(a, b)
     if a.settings.mask.kept_count == 0:
         return 0.0
-    rec = _reduce(a, None if a is b else b)
-    return _dot_from(rec, a.settings.mask.keeps_first) / (_radius(a) * _radius(b))
+    rec = _reduce(a, None if a is b else b, dc_only=_SUMS)
+    return _dot_from(rec, False) / (_radius(a) * _radius(b))
 
 
 def l2_norm(a: CompressedArray) -> float:
     """Euclidean norm sqrt(sum (F N)^2) / r (ops.py:291-297)."""
     if a.settings.mask.kept_count == 0:
         return 0.0
-    rec = _reduce(a)
-    return float(math.sqrt(max(_sq_a(rec, a.settings.mask.keeps_first), 0.0))) / _radius(a)
+    rec = _reduce(a, dc_only=_SUMS)
+    return float(math.sqrt(max(_sq_a(rec, False), 0.0))) / _radius(a)
 
 
 def mean(a: CompressedArray, padding_corrected: bool = False) -> float:

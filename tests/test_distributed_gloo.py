@@ -36,6 +36,8 @@ def np_record(a_max, a_idx, b_max, b_idx, keeps_first, dc_only):
     n = fa.shape[0]
     rec = np.zeros(16)
     rec[0] = n
+    if dc_only == 2:  # "sums" (dot / l2): every kept position goes into S_*
+        keeps_first, dc_only = False, 0
     if keeps_first and k:
         dca, dcb = fa[:, 0] * na, fb[:, 0] * nb
         ma, mb = dca.mean(), dcb.mean()

@@ -414,3 +414,12 @@ def test_elementwise_unaligned_blocks(bz, block, fk, ik, keep):
                       (bz.negate(b), o.negate(rb))):
         assert np.array_equal(got.maxima_f64().cpu().numpy(), want.maxima, equal_nan=True)
         assert np.array_equal(got.indices.cpu().numpy(), want.indices)
+    # fused subtract + l2 (the time-series step) over the same blocks; the
+    # NaN block makes the full result NaN, so also check the array without it
+    assert math.isnan(bz.subtract_l2(a, b)) and math.isnan(o.l2_norm(o.subtract(ra, rb)))
+    xb[sl(1)] = rng.normal(size=xb[sl(1)].shape)
+    rb = o.compress(o.round_to_kind(xb, fk), os_)
+    b = bz.CompressedArray(shape, s, rb.maxima, rb.indices)
+    for p_, q_, rp, rq in ((a, b, ra, rb), (b, a, rb, ra)):
+        got, want = bz.subtract_l2(p_, q_), o.l2_norm(o.subtract(rp, rq))
+        assert math.isclose(got, want, rel_tol=1e-12), (got, want)

@@ -31,8 +31,8 @@ def main(name, reps=2):
         bz.compress(x, s)
         bz.decompress(ca)
         bz.decompress(ca, kind)
-        bz.ops.moments_record(ca)
-        bz.ops.moments_record(ca, cb)
+        bz.ops.moments_record(ca, dc_only=2)
+        bz.ops.moments_record(ca, cb, dc_only=2)
         bz.ops.moments_record(ca, dc_only=True)
         bz.add(ca, cb)
         bz.negate(ca)
