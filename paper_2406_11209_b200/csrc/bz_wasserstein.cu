@@ -136,27 +136,86 @@ k_radix_hist(const unsigned long long* __restrict__ keys, int64_t n, int shift,
   hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
-// exclusive scan of m entries in place, one CTA of 1024 threads
-__global__ void __launch_bounds__(1024) k_scan_exclusive(unsigned int* __restrict__ v, int64_t m) {
-  __shared__ unsigned int part[1024];
-  const int t = threadIdx.x;
-  const int64_t per = (m + 1023) / 1024;
-  const int64_t s = t * per, e = min(m, s + per);
-  unsigned int sum = 0;
-  for (int64_t i = s; i < e; ++i) sum += v[i];
-  part[t] = sum;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
-    const unsigned int add = t >= o ? part[t - o] : 0u;
-    __syncthreads();
-    part[t] += add;
-    __syncthreads();
+// exclusive scan of m entries in place: three phases over chunks of SCH
+// entries (chunk sums, a scan of the chunk sums, chunk scans with their
+// offsets); 1024 threads x 4 consecutive entries per chunk
+constexpr int SCH = 4096;
+
+// exclusive scan of one value per thread over a CTA of 1024 threads; *total
+// receives the CTA sum
+__device__ __forceinline__ unsigned cta_exclusive_scan(unsigned x, unsigned* total) {
+  __shared__ unsigned wsum[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
   }
-  unsigned int run = t ? part[t - 1] : 0u;
-  for (int64_t i = s; i < e; ++i) {
-    const unsigned int x = v[i];
-    v[i] = run;
-    run += x;
+  __syncthreads();  // wsum reuse across calls
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    unsigned v = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    wsum[lane] = v;
+  }
+  __syncthreads();
+  *total = wsum[31];
+  return (w ? wsum[w - 1] : 0u) + inc - x;
+}
+
+__device__ __forceinline__ void load4(const unsigned* v, int64_t i, int64_t m, unsigned (&x)[4]) {
+  if (i + 4 <= m) {
+    const uint4 q = *reinterpret_cast<const uint4*>(v + i);
+    x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = i + k < m ? v[i + k] : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_reduce(const unsigned* __restrict__ v, int64_t m,
+                                                      unsigned* __restrict__ csum) {
+  unsigned x[4];
+  load4(v, (int64_t)blockIdx.x * SCH + 4 * threadIdx.x, m, x);
+  unsigned total;
+  cta_exclusive_scan(x[0] + x[1] + x[2] + x[3], &total);
+  if (threadIdx.x == 0) csum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_top(unsigned* __restrict__ csum, int nc) {
+  unsigned carry = 0;
+  for (int base = 0; base < nc; base += 1024) {
+    const int i = base + threadIdx.x;
+    const unsigned x = i < nc ? csum[i] : 0u;
+    unsigned total;
+    const unsigned e = cta_exclusive_scan(x, &total);
+    if (i < nc) csum[i] = carry + e;
+    carry += total;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_down(unsigned* __restrict__ v, int64_t m,
+                                                    const unsigned* __restrict__ csum) {
+  const int64_t i = (int64_t)blockIdx.x * SCH + 4 * threadIdx.x;
+  unsigned x[4];
+  load4(v, i, m, x);
+  unsigned total;
+  const unsigned off = csum ? csum[blockIdx.x] : 0u;  // one chunk: no chunk sums
+  unsigned run = off + cta_exclusive_scan(x[0] + x[1] + x[2] + x[3], &total);
+  unsigned y[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) { y[k] = run; run += x[k]; }
+  if (i + 4 <= m) {
+    *reinterpret_cast<uint4*>(v + i) = make_uint4(y[0], y[1], y[2], y[3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) if (i + k < m) v[i + k] = y[k];
   }
 }
 
@@ -234,6 +293,7 @@ size_t wasserstein_workspace(int64_t nblocks) {
   const int64_t nt = ntiles_of(nblocks);
   return 256 + (size_t)nblocks * 8 * 4        // pa, pb, two key buffers
          + (size_t)256 * nt * 4 + 256         // histogram / offsets
+         + ((size_t)256 * nt / SCH + 1) * 4 + 256  // chunk sums of the scan
          + (size_t)ws_::RED_CTAS * 4 * 8 + 256;
 }
 
@@ -251,12 +311,18 @@ int launch_block_means(const Geo& g, const void* maxima, const void* indices, do
 }
 
 static int radix_sort(unsigned long long* keys, unsigned long long* tmp, int64_t n,
-                      unsigned int* hist, cudaStream_t s) {
+                      unsigned int* hist, unsigned int* csum, cudaStream_t s) {
   const int nt = (int)ntiles_of(n);
   for (int pass = 0; pass < 8; ++pass) {
     const int shift = 8 * pass;
     k_radix_hist<<<nt, ws_::RT, 0, s>>>(keys, n, shift, hist, nt);
-    k_scan_exclusive<<<1, 1024, 0, s>>>(hist, (int64_t)256 * nt);
+    const int64_t m = (int64_t)256 * nt;
+    const int nc = (int)((m + SCH - 1) / SCH);
+    if (nc > 1) {
+      k_scan_reduce<<<nc, 1024, 0, s>>>(hist, m, csum);
+      k_scan_top<<<1, 1024, 0, s>>>(csum, nc);
+    }
+    k_scan_down<<<nc, 1024, 0, s>>>(hist, m, nc > 1 ? csum : nullptr);
     k_radix_scatter<<<nt, ws_::RT, 0, s>>>(keys, tmp, n, shift, hist, nt);
     if (int rc = check_launch("radix pass")) return rc;
     std::swap(keys, tmp);  // 8 passes: the result ends in the original buffer
@@ -278,6 +344,7 @@ int launch_approx_wasserstein(const Geo& ga, const Geo& gb, const void* a_max, c
   unsigned long long* t1 = reinterpret_cast<unsigned long long*>(take(n * 8));
   unsigned long long* t2 = reinterpret_cast<unsigned long long*>(take(n * 8));
   unsigned int* hist = reinterpret_cast<unsigned int*>(take((size_t)256 * ntiles_of(n) * 4));
+  unsigned int* csum = reinterpret_cast<unsigned int*>(take(((size_t)256 * ntiles_of(n) / SCH + 1) * 4));
   double* partial = reinterpret_cast<double*>(take((size_t)ws_::RED_CTAS * 4 * 8));
   double* stats = reinterpret_cast<double*>(take(64));
   int* flags = reinterpret_cast<int*>(stats + 4);
@@ -297,8 +364,8 @@ int launch_approx_wasserstein(const Geo& ga, const Geo& gb, const void* a_max, c
   k_to_keys<<<g, ws_::RT, 0, s>>>(pa, ka, n);
   k_to_keys<<<g, ws_::RT, 0, s>>>(pb, kb, n);
   if (int rc = check_launch("wasserstein prep")) return rc;
-  if (int rc = radix_sort(ka, t1, n, hist, s)) return rc;
-  if (int rc = radix_sort(kb, t2, n, hist, s)) return rc;
+  if (int rc = radix_sort(ka, t1, n, hist, csum, s)) return rc;
+  if (int rc = radix_sort(kb, t2, n, hist, csum, s)) return rc;
   k_diff_pow_partial<<<ws_::RED_CTAS, ws_::RT, 0, s>>>(ka, kb, n, order, partial);
   k_diff_pow_final<<<1, 32, 0, s>>>(partial, ws_::RED_CTAS, n, order, result);
   return check_launch("wasserstein distance");
