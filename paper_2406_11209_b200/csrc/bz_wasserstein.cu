@@ -19,8 +19,7 @@ namespace bz {
 
 namespace ws_ {
 constexpr int RT = 256;           // threads per CTA = keys per round
-constexpr int ROUNDS = 16;        // rounds per tile
-constexpr int TILE = RT * ROUNDS; // keys per tile
+constexpr int MAX_ROUNDS = 16;    // rounds per tile (fewer for small sorts: more CTAs)
 constexpr int RED_CTAS = 296;     // partial-sum CTAs (fixed: deterministic)
 }  // namespace ws_
 
@@ -120,15 +119,19 @@ __global__ void k_to_keys(const double* __restrict__ x, unsigned long long* __re
     k[i] = key_of(x[i]);
 }
 
-// hist[d * ntiles + tile]
+// Both distributions are sorted by the same launches: blockIdx.y selects the
+// array (keys / histogram / chunk sums of array y).
+// hist[y][d * ntiles + tile]
 __global__ void __launch_bounds__(ws_::RT)
-k_radix_hist(const unsigned long long* __restrict__ keys, int64_t n, int shift,
-             unsigned int* __restrict__ hist, int ntiles) {
+k_radix_hist(const unsigned long long* __restrict__ keys0, const unsigned long long* __restrict__ keys1,
+             int64_t n, int shift, unsigned int* __restrict__ hist, int ntiles, int rounds) {
+  const unsigned long long* __restrict__ keys = blockIdx.y ? keys1 : keys0;
+  hist += (int64_t)blockIdx.y * 256 * ntiles;
   __shared__ unsigned int h[256];
   h[threadIdx.x] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * ws_::TILE;
-  for (int rr = 0; rr < ws_::ROUNDS; ++rr) {
+  const int64_t base = (int64_t)blockIdx.x * ws_::RT * rounds;
+  for (int rr = 0; rr < rounds; ++rr) {
     const int64_t i = base + rr * ws_::RT + threadIdx.x;
     if (i < n) atomicAdd(&h[(unsigned)(keys[i] >> shift) & 255u], 1u);
   }
@@ -181,6 +184,8 @@ __device__ __forceinline__ void load4(const unsigned* v, int64_t i, int64_t m, u
 
 __global__ void __launch_bounds__(1024) k_scan_reduce(const unsigned* __restrict__ v, int64_t m,
                                                       unsigned* __restrict__ csum) {
+  v += (int64_t)blockIdx.y * m;
+  csum += (int64_t)blockIdx.y * gridDim.x;
   unsigned x[4];
   load4(v, (int64_t)blockIdx.x * SCH + 4 * threadIdx.x, m, x);
   unsigned total;
@@ -189,6 +194,7 @@ __global__ void __launch_bounds__(1024) k_scan_reduce(const unsigned* __restrict
 }
 
 __global__ void __launch_bounds__(1024) k_scan_top(unsigned* __restrict__ csum, int nc) {
+  csum += (int64_t)blockIdx.x * nc;  // one CTA per array
   unsigned carry = 0;
   for (int base = 0; base < nc; base += 1024) {
     const int i = base + threadIdx.x;
@@ -202,6 +208,8 @@ __global__ void __launch_bounds__(1024) k_scan_top(unsigned* __restrict__ csum, 
 
 __global__ void __launch_bounds__(1024) k_scan_down(unsigned* __restrict__ v, int64_t m,
                                                     const unsigned* __restrict__ csum) {
+  v += (int64_t)blockIdx.y * m;
+  if (csum) csum += (int64_t)blockIdx.y * gridDim.x;
   const int64_t i = (int64_t)blockIdx.x * SCH + 4 * threadIdx.x;
   unsigned x[4];
   load4(v, i, m, x);
@@ -221,17 +229,22 @@ __global__ void __launch_bounds__(1024) k_scan_down(unsigned* __restrict__ v, in
 
 // stable scatter: keys of tile `blockIdx.x` to their global positions
 __global__ void __launch_bounds__(ws_::RT)
-k_radix_scatter(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out,
-                int64_t n, int shift, const unsigned int* __restrict__ offsets, int ntiles) {
+k_radix_scatter(const unsigned long long* __restrict__ in0, const unsigned long long* __restrict__ in1,
+                unsigned long long* __restrict__ out0, unsigned long long* __restrict__ out1,
+                int64_t n, int shift, const unsigned int* __restrict__ offsets, int ntiles,
+                int rounds) {
+  const unsigned long long* __restrict__ in = blockIdx.y ? in1 : in0;
+  unsigned long long* __restrict__ out = blockIdx.y ? out1 : out0;
+  offsets += (int64_t)blockIdx.y * 256 * ntiles;
   __shared__ unsigned int run[256];
   __shared__ unsigned int wcnt[ws_::RT / 32][256];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   run[t] = offsets[(int64_t)t * ntiles + blockIdx.x];
   for (int k = 0; k < ws_::RT / 32; ++k) wcnt[k][t] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * ws_::TILE;
+  const int64_t base = (int64_t)blockIdx.x * ws_::RT * rounds;
   const unsigned lt = (1u << lane) - 1u;
-  for (int rr = 0; rr < ws_::ROUNDS; ++rr) {
+  for (int rr = 0; rr < rounds; ++rr) {
     const int64_t i = base + rr * ws_::RT + t;
     const bool valid = i < n;
     const unsigned long long key = valid ? in[i] : 0ull;
@@ -287,13 +300,20 @@ __global__ void k_diff_pow_final(const double* __restrict__ partial, int nparts,
 }
 
 // ---------------------------------------------------------------- launch --
-static int64_t ntiles_of(int64_t n) { return (n + ws_::TILE - 1) / ws_::TILE; }
+// rounds per tile: enough tiles for two CTAs per SM, at most MAX_ROUNDS
+static int rounds_of(int64_t n) {
+  return (int)std::min<int64_t>(ws_::MAX_ROUNDS, std::max<int64_t>(1, n / ((int64_t)ws_::RT * 2 * kSMs)));
+}
+static int64_t ntiles_of(int64_t n) {
+  const int64_t tile = (int64_t)ws_::RT * rounds_of(n);
+  return (n + tile - 1) / tile;
+}
 
 size_t wasserstein_workspace(int64_t nblocks) {
   const int64_t nt = ntiles_of(nblocks);
   return 256 + (size_t)nblocks * 8 * 4        // pa, pb, two key buffers
-         + (size_t)256 * nt * 4 + 256         // histogram / offsets
-         + ((size_t)256 * nt / SCH + 1) * 4 + 256  // chunk sums of the scan
+         + 2 * ((size_t)256 * nt * 4 + 256)         // histograms / offsets, per array
+         + 2 * ((size_t)256 * nt / SCH + 1) * 4 + 256  // chunk sums of the scans
          + (size_t)ws_::RED_CTAS * 4 * 8 + 256;
 }
 
@@ -310,22 +330,25 @@ int launch_block_means(const Geo& g, const void* maxima, const void* indices, do
   return check_launch("block_means");
 }
 
-static int radix_sort(unsigned long long* keys, unsigned long long* tmp, int64_t n,
-                      unsigned int* hist, unsigned int* csum, cudaStream_t s) {
-  const int nt = (int)ntiles_of(n);
+// sorts ka and kb (n keys each) together; the results end in ka / kb
+static int radix_sort2(unsigned long long* ka, unsigned long long* kb, unsigned long long* ta,
+                       unsigned long long* tb, int64_t n, unsigned int* hist, unsigned int* csum,
+                       cudaStream_t s) {
+  const int nt = (int)ntiles_of(n), rounds = rounds_of(n);
+  const int64_t m = (int64_t)256 * nt;
+  const int nc = (int)((m + SCH - 1) / SCH);
   for (int pass = 0; pass < 8; ++pass) {
     const int shift = 8 * pass;
-    k_radix_hist<<<nt, ws_::RT, 0, s>>>(keys, n, shift, hist, nt);
-    const int64_t m = (int64_t)256 * nt;
-    const int nc = (int)((m + SCH - 1) / SCH);
+    k_radix_hist<<<dim3(nt, 2), ws_::RT, 0, s>>>(ka, kb, n, shift, hist, nt, rounds);
     if (nc > 1) {
-      k_scan_reduce<<<nc, 1024, 0, s>>>(hist, m, csum);
-      k_scan_top<<<1, 1024, 0, s>>>(csum, nc);
+      k_scan_reduce<<<dim3(nc, 2), 1024, 0, s>>>(hist, m, csum);
+      k_scan_top<<<2, 1024, 0, s>>>(csum, nc);
     }
-    k_scan_down<<<nc, 1024, 0, s>>>(hist, m, nc > 1 ? csum : nullptr);
-    k_radix_scatter<<<nt, ws_::RT, 0, s>>>(keys, tmp, n, shift, hist, nt);
+    k_scan_down<<<dim3(nc, 2), 1024, 0, s>>>(hist, m, nc > 1 ? csum : nullptr);
+    k_radix_scatter<<<dim3(nt, 2), ws_::RT, 0, s>>>(ka, kb, ta, tb, n, shift, hist, nt, rounds);
     if (int rc = check_launch("radix pass")) return rc;
-    std::swap(keys, tmp);  // 8 passes: the result ends in the original buffer
+    std::swap(ka, ta);  // 8 passes: the results end in the original buffers
+    std::swap(kb, tb);
   }
   return BZ_OK;
 }
@@ -343,8 +366,8 @@ int launch_approx_wasserstein(const Geo& ga, const Geo& gb, const void* a_max, c
   unsigned long long* kb = reinterpret_cast<unsigned long long*>(pb);
   unsigned long long* t1 = reinterpret_cast<unsigned long long*>(take(n * 8));
   unsigned long long* t2 = reinterpret_cast<unsigned long long*>(take(n * 8));
-  unsigned int* hist = reinterpret_cast<unsigned int*>(take((size_t)256 * ntiles_of(n) * 4));
-  unsigned int* csum = reinterpret_cast<unsigned int*>(take(((size_t)256 * ntiles_of(n) / SCH + 1) * 4));
+  unsigned int* hist = reinterpret_cast<unsigned int*>(take(2 * (size_t)256 * ntiles_of(n) * 4));
+  unsigned int* csum = reinterpret_cast<unsigned int*>(take(2 * ((size_t)256 * ntiles_of(n) / SCH + 1) * 4));
   double* partial = reinterpret_cast<double*>(take((size_t)ws_::RED_CTAS * 4 * 8));
   double* stats = reinterpret_cast<double*>(take(64));
   int* flags = reinterpret_cast<int*>(stats + 4);
@@ -364,8 +387,7 @@ int launch_approx_wasserstein(const Geo& ga, const Geo& gb, const void* a_max, c
   k_to_keys<<<g, ws_::RT, 0, s>>>(pa, ka, n);
   k_to_keys<<<g, ws_::RT, 0, s>>>(pb, kb, n);
   if (int rc = check_launch("wasserstein prep")) return rc;
-  if (int rc = radix_sort(ka, t1, n, hist, csum, s)) return rc;
-  if (int rc = radix_sort(kb, t2, n, hist, csum, s)) return rc;
+  if (int rc = radix_sort2(ka, kb, t1, t2, n, hist, csum, s)) return rc;
   k_diff_pow_partial<<<ws_::RED_CTAS, ws_::RT, 0, s>>>(ka, kb, n, order, partial);
   k_diff_pow_final<<<1, 32, 0, s>>>(partial, ws_::RED_CTAS, n, order, result);
   return check_launch("wasserstein distance");
