@@ -129,7 +129,7 @@ int bz_add_scalar(const bz_layout* L, const void* maxima, const void* indices, d
  * over every kept position.  Records of shards merge with Chan's formulas.
  * `pair` = 0 reads only a (b ignored; *_b and *_ab mirror a).
  * dc_only = 1 computes entries 0-5 from the first coefficient only (mean).
- * dc_only = 2 ("sums", dot / l2): entries 0-5 are 0 and S_* run over every
+ * dc_only = 2 ("sums", dot / l2): entries 1-5 are 0 and S_* run over every
  * kept position, the first included -- no per-block DC moments.
  * The workspace must be zero-filled before its first use; the kernels leave
  * it re-armed, so a caller keeps one workspace per stream.                  */

@@ -374,8 +374,9 @@ struct ChunkPos {
 };
 
 // FK >= 0: both operands' maxima are of float kind FK (compile time);
-// SPAN = false: K is a multiple of V, no chunk crosses a block boundary
-template <typename IT, int NW, int U, bool PAIR, int FK, bool SPAN>
+// SPAN = false: K is a multiple of V, no chunk crosses a block boundary;
+// DC = false: no DC moments at all (keeps_first == 0 or the "sums" mode)
+template <typename IT, int NW, int U, bool PAIR, int FK, bool SPAN, bool DC = true>
 __global__ void __launch_bounds__(256, 2)
 k_moments_stream(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
                  const void* __restrict__ a_max, const IT* __restrict__ a_idx,
@@ -387,7 +388,7 @@ k_moments_stream(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
   const int64_t nchunks = total / V;  // whole chunks (tail below)
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const bool dc = keeps_first != 0;
+  const bool dc = DC && keeps_first != 0;
   MomState st;
   const unsigned char* ca = reinterpret_cast<const unsigned char*>(a_idx);
   const unsigned char* cb = reinterpret_cast<const unsigned char*>(b_idx);
@@ -641,7 +642,8 @@ static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const v
 #define BZ_MS(NWV, FKV, SP)                                                                      \
   {                                                                                              \
     constexpr int UU = NWV == 8 ? U / 2 : U;                                                     \
-    auto kern = k_moments_stream<IT, NWV, UU, PAIR, FKV, SP>;                                    \
+    auto kern = kf ? k_moments_stream<IT, NWV, UU, PAIR, FKV, SP, true>                          \
+                   : k_moments_stream<IT, NWV, UU, PAIR, FKV, SP, false>;                        \
     const int grid = persistent_grid(kern, 256, 0, (chunks + 256 * UU - 1) / (256 * UU));       \
     kern<<<grid, 256, 0, s>>>(B, kept, kf, ga.float_kind, gb.float_kind, a_max,                  \
                               (const IT*)a_idx, b_max, (const IT*)b_idx, ws, record);            \
