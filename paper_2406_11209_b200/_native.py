@@ -8,6 +8,7 @@ CUDA device is missing, every compute entry point raises ``NativeUnavailable``.
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 import threading
 
@@ -138,6 +139,31 @@ def call(name: str, *args) -> int:
 
 def query(name: str, *args):
     return getattr(load_library(), name)(*args)
+
+
+def _device_of(x):
+    dev = getattr(x, "device", None)
+    if dev is None:
+        vals = getattr(x, "values", None)
+        dev = getattr(vals, "device", None)
+    return dev
+
+
+def on_device(fn):
+    """Run a public operator with its first operand's GPU current, so the
+    library's launches, occupancy queries and attribute calls (which act on
+    the current device) target the device that holds the data."""
+
+    @functools.wraps(fn)
+    def wrapper(a, *args, **kwargs):
+        dev = _device_of(a)
+        if dev is not None and dev.type == "cuda" and dev.index is not None \
+                and dev.index != torch.cuda.current_device():
+            with torch.cuda.device(dev):
+                return fn(a, *args, **kwargs)
+        return fn(a, *args, **kwargs)
+
+    return wrapper
 
 
 def ptr(t: torch.Tensor | None) -> int | None:

@@ -236,7 +236,7 @@ class CompressedArray:
     operand's unchanged maxima or indices (negate, mul_scalar).
     """
 
-    __slots__ = ("original_shape", "settings", "maxima", "indices")
+    __slots__ = ("original_shape", "settings", "maxima", "indices", "_lay")
 
     def __init__(self, original_shape, settings: CodecSettings, maxima, indices, *,
                  _trusted: bool = False):
@@ -283,7 +283,12 @@ class CompressedArray:
         return self.maxima.view(pattern_dtype(self.settings.float_kind))
 
     def layout(self) -> _native.Layout:
-        return layout(self.settings, self.original_shape, self.device)
+        """The C-ABI descriptor, built once per array (the array is immutable)."""
+        L = getattr(self, "_lay", None)
+        if L is None:
+            L = layout(self.settings, self.original_shape, self.device)
+            object.__setattr__(self, "_lay", L)
+        return L
 
     def __eq__(self, other):
         if not isinstance(other, CompressedArray):
@@ -318,6 +323,7 @@ def _to_index_storage(values, kind: IndexKind, device) -> torch.Tensor:
 
 
 # ------------------------------------------------------------------ codec ----
+@_native.on_device
 def compress(a: DenseArray, settings: CodecSettings) -> CompressedArray:
     """convert -> block -> transform -> bin -> prune (codec.py:321-334), fused."""
     if a.ndim != settings.ndim:
@@ -337,6 +343,7 @@ def compress(a: DenseArray, settings: CodecSettings) -> CompressedArray:
     return CompressedArray(a.shape, settings, maxima, indices, _trusted=True)
 
 
+@_native.on_device
 def decompress(a: CompressedArray, out_kind: FloatKind = FloatKind.F64) -> DenseArray:
     """Inverse transform, *N, /r, merge, crop (codec.py:364-384), fused.
 
@@ -417,6 +424,7 @@ def unflatten(flat, mask: PruningMask) -> torch.Tensor:
     return out
 
 
+@_native.on_device
 def specified_coefficients(a: CompressedArray) -> BlockedArray:
     """(F * N) / r per kept position, zeros elsewhere (codec.py:337-361)."""
     out = torch.empty(a.block_grid + a.settings.block_shape, dtype=torch.float64, device=a.device)

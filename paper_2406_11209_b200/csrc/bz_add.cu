@@ -331,7 +331,7 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
         }
       }
     }
-    if (RED) red_acc = __fma_rn((double)red_sq, n * n, red_acc);
+    if (RED) red_acc = __fma_rn((double)red_sq * n, n, red_acc);
   }
   if constexpr (RED) red_finish(red_acc, red_ws);
 }
@@ -430,6 +430,46 @@ k_add_staged(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
     __syncthreads();
     smem_to_tile(reinterpret_cast<unsigned char*>(out_idx) + byte0, so, nbytes, miso, t, 256);
     __syncthreads();  // tiles reused
+  }
+}
+
+// ------------------------------------------ general add (any block size) --
+// Blocks too large for the register-held layouts above (e.g. I64 indices
+// with 8x8x8 full masks, I32 32x32 blocks): a warp per block, run-time float
+// kinds, two passes over the block (the second re-reads through L1/L2), IEEE
+// division and exact binning -- codec.py:337-350 / 253-278 verbatim.
+template <typename IT, int MODE>
+__global__ void __launch_bounds__(256)
+k_add_general(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
+              const void* __restrict__ a_max, const IT* __restrict__ a_idx,
+              const void* __restrict__ b_max, const IT* __restrict__ b_idx, int subtract,
+              double shift, void* __restrict__ out_max, IT* __restrict__ out_idx) {
+  constexpr int IK = sizeof(IT) == 1 ? BZ_I8 : sizeof(IT) == 2 ? BZ_I16 : sizeof(IT) == 4 ? BZ_I32 : BZ_I64;
+  const double r = radius_f64(IK), bound = clamp_bound_f64(IK);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = warp; b < nblocks; b += nwarps) {
+    const int64_t base = b * (int64_t)kept;
+    const double na = load_kind_rt(a_max, b, fk_a);
+    const double nb = MODE == 0 ? load_kind_rt(b_max, b, fk_b) : 0.0;
+    auto coeff = [&](int k) -> double {
+      const double xa = __ddiv_rn(__dmul_rn((double)a_idx[base + k], na), r);
+      if (MODE == 0) {
+        const double fb = subtract ? -(double)b_idx[base + k] : (double)b_idx[base + k];
+        return __dadd_rn(xa, __ddiv_rn(__dmul_rn(fb, nb), r));
+      }
+      return k == 0 ? __dadd_rn(xa, shift) : xa;
+    };
+    double m = 0.0;
+    for (int k = lane; k < kept; k += 32) m = nanmax_abs(m, coeff(k));
+    for (int o = 16; o > 0; o >>= 1) {
+      const double t = __shfl_xor_sync(0xffffffffu, m, o);
+      m = (isnan(t) || isnan(m)) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(m, t);
+    }
+    const double n = round_to_kind_rt(m, fk_out);
+    if (lane == 0) store_kind_rt(out_max, b, n, fk_out);
+    for (int k = lane; k < kept; k += 32) out_idx[base + k] = (IT)bin_exact(coeff(k), n, r, bound);
   }
 }
 
@@ -556,7 +596,7 @@ k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
             if constexpr (sizeof(IT) == 1) sq += q[j] * q[j];
             else sq64 += (long long)(q[j] * q[j]);
           }
-        red_acc = __fma_rn((double)(sq64 + sq), n * n, red_acc);
+        red_acc = __fma_rn((double)(sq64 + sq) * n, n, red_acc);
       } else {
 #pragma unroll
         for (int j = 0; j < CPL; ++j)
@@ -584,7 +624,20 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
   } else {
     while (GS < 32 && GS < vecs) GS <<= 1;
     NCH = (vecs + GS - 1) / GS;
-    if (NCH > 4) { set_error("add: kept block too large (%d indices)", kept); return BZ_E_UNSUPPORTED; }
+    if (NCH > 4) {  // too large to hold in registers: the general warp-per-block kernel
+      const int g = grid_for(ga.nblocks * 32, 256, 4);
+      if (mode == 0)
+        k_add_general<IT, 0><<<g, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind, gb.float_kind,
+                                               ga.float_kind, a_max, (const IT*)a_idx, b_max,
+                                               (const IT*)b_idx, subtract, shift, out_max,
+                                               (IT*)out_idx);
+      else
+        k_add_general<IT, 1><<<g, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind, gb.float_kind,
+                                               ga.float_kind, a_max, (const IT*)a_idx, b_max,
+                                               (const IT*)b_idx, subtract, shift, out_max,
+                                               (IT*)out_idx);
+      return check_launch("add_general");
+    }
     NCH = NCH <= 1 ? 1 : (NCH <= 2 ? 2 : 4);
   }
   const bool vec = ((kept * sizeof(IT)) % 16 == 0) &&

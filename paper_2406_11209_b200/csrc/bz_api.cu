@@ -57,6 +57,17 @@ static int need_matrices(const bz_layout* L) {
   return BZ_OK;
 }
 
+// two operands walked block by block together: same block count, kept
+// count, first-coefficient flag and index kind (a C caller passing layouts
+// of different grids would otherwise read past b's buffers)
+static int check_pair(const bz_layout* La, const bz_layout* Lb, const char* what,
+                      bool same_index_kind) {
+  if (block_count(La) != block_count(Lb)) { set_error("%s: block counts differ", what); return BZ_E_INVALID; }
+  if (La->kept != Lb->kept || La->keeps_first != Lb->keeps_first) { set_error("%s: masks differ", what); return BZ_E_INVALID; }
+  if (same_index_kind && La->index_kind != Lb->index_kind) { set_error("%s: index kinds differ (convert first)", what); return BZ_E_INVALID; }
+  return BZ_OK;
+}
+
 }  // namespace bz
 
 using namespace bz;
@@ -152,7 +163,7 @@ int bz_add(const bz_layout* La, const bz_layout* Lb, const void* a_max, const vo
            void* stream) {
   if (int rc = validate(La)) return rc;
   if (int rc = validate(Lb)) return rc;
-  if (La->index_kind != Lb->index_kind || La->kept != Lb->kept) { set_error("add: incompatible operands"); return BZ_E_INVALID; }
+  if (int rc = check_pair(La, Lb, "add", true)) return rc;
   return launch_add(make_geo(La), make_geo(Lb), a_max, a_idx, b_max, b_idx, subtract, 0.0, 0,
                     out_max, out_idx, S(stream));
 }
@@ -164,7 +175,7 @@ int bz_subtract_l2(const bz_layout* La, const bz_layout* Lb, const void* a_max, 
                    void* stream) {
   if (int rc = validate(La)) return rc;
   if (int rc = validate(Lb)) return rc;
-  if (La->index_kind != Lb->index_kind || La->kept != Lb->kept) { set_error("subtract_l2: incompatible operands"); return BZ_E_INVALID; }
+  if (int rc = check_pair(La, Lb, "subtract_l2", true)) return rc;
   return launch_subtract_l2(make_geo(La), make_geo(Lb), a_max, a_idx, b_max, b_idx, out, ws,
                             ws_bytes, S(stream));
 }
@@ -190,8 +201,7 @@ int bz_moments(const bz_layout* La, const bz_layout* Lb, const void* a_max, cons
   const bz_layout* lb = pair ? Lb : La;
   if (pair) {
     if (int rc = validate(Lb)) return rc;
-    if (La->index_kind != Lb->index_kind) { set_error("moments: index kinds differ (convert first)"); return BZ_E_INVALID; }
-    if (La->kept != Lb->kept) { set_error("moments: masks differ"); return BZ_E_INVALID; }
+    if (int rc = check_pair(La, Lb, "moments", true)) return rc;
   }
   return launch_moments(make_geo(La), make_geo(lb), a_max, a_idx, pair ? b_max : a_max,
                         pair ? b_idx : a_idx, pair, dc_only, record, ws, ws_bytes, S(stream));

@@ -77,10 +77,10 @@ struct MomState {
   template <bool PAIR = true>
   __device__ __forceinline__ void add_block(double iab, double iaa, double ibb, double fa0,
                                             double fb0, double na, double nb, bool dc) {
-    Saa = __fma_rn(iaa, na * na, Saa);
+    Saa = __fma_rn(iaa * na, na, Saa);  // (i*N)*N: an all-zero segment adds 0 even when N*N overflows
     if (PAIR) {
-      Sab = __fma_rn(iab, na * nb, Sab);
-      Sbb = __fma_rn(ibb, nb * nb, Sbb);
+      Sab = __fma_rn(iab * na, nb, Sab);
+      Sbb = __fma_rn(ibb * nb, nb, Sbb);
     }
     if (dc) {
       const double dca = fa0 * na;
@@ -103,10 +103,10 @@ struct MomState {
   // AC part of one block segment (linear: segments may be added separately)
   template <bool PAIR = true>
   __device__ __forceinline__ void add_ac(double iab, double iaa, double ibb, double na, double nb) {
-    Saa = __fma_rn(iaa, na * na, Saa);
+    Saa = __fma_rn(iaa * na, na, Saa);  // (i*N)*N: an all-zero segment adds 0 even when N*N overflows
     if (PAIR) {
-      Sab = __fma_rn(iab, na * nb, Sab);
-      Sbb = __fma_rn(ibb, nb * nb, Sbb);
+      Sab = __fma_rn(iab * na, nb, Sab);
+      Sbb = __fma_rn(ibb * nb, nb, Sbb);
     }
   }
   // once per block: its DC value (when the mask keeps it) and the block count

@@ -8,7 +8,8 @@ elementwise operator are shard-local (blocks are independent,
 PAPER.md:295) -- no communication.  A reduction computes the shard's partial
 record with the fused ``bz_moments`` kernel, all-gathers the P records
 (P x 16 float64 -- the only data that crosses NVLink) and merges them in rank
-order with Chan's formulas, so every rank returns the same value.  The
+order with Chan's formulas, so every rank returns the same value (one
+all_gather_into_tensor and one device->host copy per reduction).  The
 concatenation of the shards' maxima / indices along axis 0 is exactly the
 unsharded CompressedArray.
 """
@@ -24,7 +25,7 @@ from .codec import CodecSettings, CompressedArray, compress as _compress
 from .ops import Record, merge_records, moments_record
 
 __all__ = ["block_rows", "shard_slab", "ShardedCompressedArray", "compress_sharded",
-           "gather_records"]
+           "gather_records", "allgather_sum"]
 
 
 def block_rows(g0: int, rank: int, world: int) -> tuple[int, int]:
@@ -41,11 +42,24 @@ def shard_slab(global_shape, block_shape, rank: int, world: int) -> tuple[int, i
 
 
 def gather_records(rec: torch.Tensor, group=None) -> list[Record]:
-    """All-gather one record per rank (NCCL on GPU tensors, gloo on CPU)."""
+    """One collective per reduction: all-gather every rank's 16-double record
+    into one (P*16) tensor (NCCL over NVLink on GPU tensors, gloo on CPU),
+    then ONE device->host copy; the P records are merged on the host in rank
+    order (P <= 8 records -- microseconds)."""
     world = dist.get_world_size(group)
-    out = [torch.empty_like(rec) for _ in range(world)]
-    dist.all_gather(out, rec.contiguous(), group=group)
-    return [Record.from_array(t.cpu().numpy()) for t in out]
+    flat = rec.contiguous().reshape(-1)
+    out = torch.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)
+    dist.all_gather_into_tensor(out, flat, group=group)
+    host = out.cpu().numpy().reshape(world, -1)
+    return [Record.from_array(host[r]) for r in range(world)]
+
+
+def allgather_sum(x: torch.Tensor, group=None) -> float:
+    """Sum of one double per rank, added in rank order (deterministic)."""
+    world = dist.get_world_size(group)
+    out = torch.empty(world, dtype=torch.float64, device=x.device)
+    dist.all_gather_into_tensor(out, x.reshape(1).to(torch.float64), group=group)
+    return float(sum(float(v) for v in out.cpu().numpy()))
 
 
 class ShardedCompressedArray(CompressedArray):
@@ -74,6 +88,9 @@ class ShardedCompressedArray(CompressedArray):
         other = None if b is None or b is self else b
         rec = self._record_fn(self, other, dc_only)
         return merge_records(gather_records(rec, self.group))
+
+    def _reduce_sum(self, x: torch.Tensor) -> float:
+        return allgather_sum(x, self.group)
 
     @property
     def local(self) -> CompressedArray:

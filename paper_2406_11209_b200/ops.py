@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -115,6 +116,7 @@ def _derive(a: CompressedArray, maxima, indices) -> CompressedArray:
 
 
 # ----------------------------------------------------------- elementwise ----
+@_native.on_device
 def negate(a: CompressedArray) -> CompressedArray:
     """{s, N, -F}; exact (ops.py:195-197).  Maxima are shared."""
     out = torch.empty_like(a.indices)
@@ -136,16 +138,19 @@ def _add(a: CompressedArray, b: CompressedArray, subtract: int) -> CompressedArr
     return _derive(a, out_max, out_idx)
 
 
+@_native.on_device
 def add(a: CompressedArray, b: CompressedArray) -> CompressedArray:
     """Elementwise sum with rebinning under a's kinds (ops.py:200-204); bit-exact."""
     return _add(a, b, 0)
 
 
+@_native.on_device
 def subtract(a: CompressedArray, b: CompressedArray) -> CompressedArray:
     """a - b == add(a, negate(b)) bit for bit, in one pass."""
     return _add(a, b, 1)
 
 
+@_native.on_device
 def add_scalar(a: CompressedArray, x: float) -> CompressedArray:
     """Shift each block's first coefficient by x*sqrt(prod i), rebin (ops.py:207-215)."""
     _require_first_coefficient(a)
@@ -158,6 +163,7 @@ def add_scalar(a: CompressedArray, x: float) -> CompressedArray:
     return _derive(a, out_max, out_idx)
 
 
+@_native.on_device
 def mul_scalar(a: CompressedArray, x: float) -> CompressedArray:
     """N' = RN_kind(N*|x|), F' = F*sign(x) (ops.py:218-223).  x > 0 shares F."""
     x = float(x)
@@ -221,11 +227,17 @@ def merge_records(records) -> Record:
 
 
 _REDUCE_WS: dict = {}
+_MOMENTS_WS_BYTES: list = []
 
 
-def _reduce_workspace(dev: torch.device, nbytes: int) -> torch.Tensor:
+def _reduce_workspace(dev: torch.device, La) -> torch.Tensor:
     """Zero-initialised, persistent per (device, stream) workspace: the
-    reduction kernels leave their ticket counter re-armed (include/bzc_b200.h)."""
+    reduction kernels leave their ticket counter re-armed (include/bzc_b200.h).
+    Calls on one stream are ordered on the GPU, so threads sharing a stream
+    may share it."""
+    if not _MOMENTS_WS_BYTES:  # the size depends on no layout field
+        _MOMENTS_WS_BYTES.append(int(_native.query("bz_moments_workspace", ctypes.byref(La))))
+    nbytes = _MOMENTS_WS_BYTES[0]
     key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
     ws = _REDUCE_WS.get(key)
     if ws is None or ws.numel() < nbytes:
@@ -235,11 +247,14 @@ def _reduce_workspace(dev: torch.device, nbytes: int) -> torch.Tensor:
 
 
 def moments_record(a: CompressedArray, b: CompressedArray | None = None, *,
-                   dc_only: int = 0) -> torch.Tensor:
-    """Launch the fused reduction; returns the device record (16 float64)."""
+                   dc_only: int = 0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Launch the fused reduction; returns the record (16 float64) -- a new
+    device tensor, or ``out`` (device memory or pinned host memory, which the
+    kernel's last CTA writes directly)."""
     pair = b is not None and b is not a
     dev = a.device
-    rec = torch.empty(_native.RECORD_DOUBLES, dtype=torch.float64, device=dev)
+    rec = out if out is not None else torch.empty(_native.RECORD_DOUBLES, dtype=torch.float64,
+                                                  device=dev)
     La = a.layout()
     Lb = b.layout() if pair else La
     bm = bi = None
@@ -250,7 +265,11 @@ def moments_record(a: CompressedArray, b: CompressedArray | None = None, *,
             # mixed index kinds are legal for reductions (ops.py:100-116): widen
             wide = max(a.settings.index_kind, b.settings.index_kind, key=lambda k: k.bits)
             if a.settings.index_kind is not wide:
-                return moments_record(b, a, dc_only=dc_only)[[0, 2, 1, 3, 5, 4, 6, 8, 7, 9, 10, 11, 12, 13, 14, 15]]
+                swapped = moments_record(b, a, dc_only=dc_only)[_SWAP_AB]
+                if out is None:
+                    return swapped
+                out.copy_(swapped)
+                return out
             conv = torch.empty(bi.shape, dtype=wide.torch_dtype, device=dev)
             _native.call("bz_convert_indices", bi.data_ptr(), b.settings.index_kind.code,
                          conv.data_ptr(), wide.code, bi.numel(), _stream(a))
@@ -258,26 +277,38 @@ def moments_record(a: CompressedArray, b: CompressedArray | None = None, *,
             from .codec import layout as _layout
 
             Lb = _layout(b.settings, b.original_shape, dev, index_kind=wide)
-    ws = _reduce_workspace(dev, _native.query("bz_moments_workspace", ctypes.byref(La)))
-    _native.call("bz_moments", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
-                 a.indices.data_ptr(), bm.data_ptr() if pair else None,
-                 bi.data_ptr() if pair else None, int(pair), int(dc_only), rec.data_ptr(),
-                 ws.data_ptr(), ws.numel(), _stream(a))
+    ws = _reduce_workspace(dev, La)
+    try:
+        _native.call("bz_moments", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
+                     a.indices.data_ptr(), bm.data_ptr() if pair else None,
+                     bi.data_ptr() if pair else None, int(pair), int(dc_only), rec.data_ptr(),
+                     ws.data_ptr(), ws.numel(), _stream(a))
+    except _native.NativeError:
+        ws.zero_()  # never leave a half-counted ticket behind a failed launch
+        raise
     return rec
 
 
-_HOST_REC: dict = {}
+_SWAP_AB = [0, 2, 1, 3, 5, 4, 6, 8, 7, 9, 10, 11, 12, 13, 14, 15]
+_TLS = threading.local()
+
+
+def _host_record() -> torch.Tensor:
+    """This thread's pinned record buffer (device-addressable under UVA):
+    concurrent reductions from several threads never share one."""
+    h = getattr(_TLS, "rec", None)
+    if h is None:
+        h = torch.empty(_native.RECORD_DOUBLES, dtype=torch.float64, pin_memory=True)
+        _TLS.rec = h
+    return h
 
 
 def record_to_host(rec: torch.Tensor) -> np.ndarray:
-    """Copy a device record through a pinned buffer, waiting on the current
-    stream only (a pageable .cpu() copy would stall other streams' copies)."""
+    """Copy a device record through this thread's pinned buffer, waiting on
+    the current stream only (a pageable .cpu() copy would stall other
+    streams' copies)."""
     dev = rec.device
-    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
-    h = _HOST_REC.get(key)
-    if h is None:
-        h = torch.empty(rec.numel(), dtype=rec.dtype, pin_memory=True)
-        _HOST_REC[key] = h
+    h = _host_record()
     h.copy_(rec, non_blocking=True)
     torch.cuda.current_stream(dev).synchronize()
     return h.numpy().copy()
@@ -293,7 +324,9 @@ def _reduce(a, b=None, *, dc_only=False) -> Record:
     hook = getattr(a, "_reduce_record", None)
     if hook is not None:
         return hook(b, dc_only)
-    return Record.from_array(record_to_host(moments_record(a, b, dc_only=dc_only)))
+    h = moments_record(a, b, dc_only=dc_only, out=_host_record())
+    torch.cuda.current_stream(a.device).synchronize()
+    return Record.from_array(h.numpy())
 
 
 def _radius(a) -> float:
@@ -323,6 +356,7 @@ def _sq_b(rec: Record, keeps_first: bool) -> float:
     return rec.s_bb + dc
 
 
+@_native.on_device
 def dot(a: CompressedArray, b: CompressedArray) -> float:
     """Dot product of the underlying arrays (ops.py:226-241)."""
     _check_compatible(a, b)
@@ -332,6 +366,7 @@ def dot(a: CompressedArray, b: CompressedArray) -> float:
     return _dot_from(rec, False) / (_radius(a) * _radius(b))
 
 
+@_native.on_device
 def l2_norm(a: CompressedArray) -> float:
     """Euclidean norm sqrt(sum (F N)^2) / r (ops.py:291-297)."""
     if a.settings.mask.kept_count == 0:
@@ -340,6 +375,7 @@ def l2_norm(a: CompressedArray) -> float:
     return float(math.sqrt(max(_sq_a(rec, False), 0.0))) / _radius(a)
 
 
+@_native.on_device
 def mean(a: CompressedArray, padding_corrected: bool = False) -> float:
     """Mean from the first coefficients (ops.py:244-257)."""
     _require_first_coefficient(a)
@@ -355,6 +391,7 @@ def _cov_from(rec_m: float, rec_s: float, a, b) -> float:
     return (rec_m + rec_s) / (_radius(a) * _radius(b)) / (_global_blocks(a) * a.settings.block_size)
 
 
+@_native.on_device
 def covariance(a: CompressedArray, b: CompressedArray) -> float:
     """Population covariance over the padded count (ops.py:260-283)."""
     _check_compatible(a, b)
@@ -369,6 +406,7 @@ def variance(a: CompressedArray) -> float:
     return covariance(a, a)
 
 
+@_native.on_device
 def cosine_similarity(a: CompressedArray, b: CompressedArray) -> float:
     """dot / (|a| |b|); ZeroNormOperand on a zero norm (ops.py:300-306).  One pass."""
     _check_compatible(a, b)
@@ -391,6 +429,7 @@ def _signed_power(base: float, weight: float, term: str) -> float:
     return float(base) ** float(weight)
 
 
+@_native.on_device
 def ssim_components(a: CompressedArray, b: CompressedArray,
                     params: SsimParams | None = None) -> tuple[float, float, float]:
     """Luminance, contrast, structure (ops.py:317-335), from one fused pass."""
@@ -426,6 +465,7 @@ def ssim(a: CompressedArray, b: CompressedArray, params: SsimParams | None = Non
 _SL2_WS: dict = {}
 
 
+@_native.on_device
 def _subtract_l2_sq(a: CompressedArray, b: CompressedArray, out: torch.Tensor) -> bool:
     """Squared L2 norm of subtract(a, b) into the device double ``out`` with
     the fused kernel (bz_subtract_l2); False when no fused kernel serves the
@@ -452,12 +492,17 @@ def _subtract_l2_sq(a: CompressedArray, b: CompressedArray, out: torch.Tensor) -
     return True
 
 
+@_native.on_device
 def subtract_l2(a: CompressedArray, b: CompressedArray) -> float:
     """l2_norm(subtract(a, b)) in one fused pass (cli.py:240-243); the same
     value as materialising the difference (rebinned under a's settings)."""
-    if getattr(a, "_reduce_record", None) is not None:  # sharded: compose
-        return l2_norm(subtract(a, b))
     out = torch.empty(1, dtype=torch.float64, device=a.device)
+    sharded = getattr(a, "_reduce_sum", None)
+    if sharded is not None:
+        # each shard's fused squared norm, summed across ranks in rank order
+        if not _subtract_l2_sq(a, b, out):
+            return l2_norm(subtract(a, b))
+        return float(math.sqrt(max(sharded(out), 0.0))) / _radius(a)
     if not _subtract_l2_sq(a, b, out):
         return l2_norm(subtract(a, b))
     return float(math.sqrt(max(float(out.item()), 0.0))) / _radius(a)
@@ -504,6 +549,7 @@ class WassersteinParams:
             raise ValueError("normalization tolerance must be non-negative")
 
 
+@_native.on_device
 def block_means(a: CompressedArray) -> torch.Tensor:
     """Per-block means, flattened in row-major grid order (ops.py:355-359):
     F0 * N / r / sqrt(block size), the reference's op order; f64 on the GPU."""
@@ -518,6 +564,7 @@ def block_means(a: CompressedArray) -> torch.Tensor:
 _WS_W: dict = {}
 
 
+@_native.on_device
 def approx_wasserstein(a: CompressedArray, b: CompressedArray,
                        params: WassersteinParams | None = None) -> float:
     """Order-p distance between the sorted block-mean distributions
