@@ -31,6 +31,7 @@
 // contiguous run of 2K bytes per warp tile.
 #include "bz_fast.cuh"
 #include "bz_kernels.cuh"
+#include "bz_tma.cuh"
 
 #include <cstdlib>
 
@@ -89,6 +90,113 @@ __device__ __forceinline__ void idct4(double* v, const Dct4K& K) {
 }
 }  // namespace d4
 
+// Everything after a warp's two blocks are in registers (v[a0*4 + a3] at
+// (a1, a2) = (i1, i2) of block b): axes 0 and 3, the warp-local exchange,
+// axes 1 and 2, maximum, binning, staging and the contiguous copy-out of
+// the pair's kept indices (blocks b0, b0 + 1).  Shared by the cp.async and
+// the TMA kernels.
+struct Ctx4 {
+  int lane, bs, o;
+  int K;
+  int64_t nblocks;
+  d4::Dct4K KC;
+  double* wbase;  // phase A write base of this lane
+  double* rbase;  // phase B read base of this lane
+  int8_t* stg;    // the warp's output staging (2 x SS bytes)
+  int8_t* sbase;  // this block's staging run (stg + bs*K)
+};
+
+template <int FK>
+__device__ __forceinline__ void dct4_compress_pair(double (&v)[16], const int16_t (&rk)[16],
+                                                   const Ctx4& cx, int64_t b0,
+                                                   int64_t b, bool valid,
+                                                   void* __restrict__ maxima,
+                                                   int8_t* __restrict__ indices,
+                                                   int32_t* __restrict__ list,
+                                                   int32_t* __restrict__ count) {
+  using namespace d4;
+  const int lane = cx.lane, bs = cx.bs, o = cx.o, K = cx.K;
+  const Dct4K KC = cx.KC;
+  double* wbase = cx.wbase;
+  double* rbase = cx.rbase;
+  int8_t* stg = cx.stg;
+  int8_t* sbase = cx.sbase;
+  constexpr int ZS = 2 * BS;
+  struct { int64_t nblocks; } f{cx.nblocks};
+#pragma unroll
+  for (int a3 = 0; a3 < 4; ++a3) fdct4<4>(v + a3, KC);  // axis 0
+#pragma unroll
+  for (int a0 = 0; a0 < 4; ++a0) fdct4<1>(v + a0 * 4, KC);  // axis 3
+#pragma unroll
+  for (int a0 = 0; a0 < 4; ++a0)
+#pragma unroll
+    for (int a3 = 0; a3 < 4; ++a3) wbase[xoff(a0, 0, 0, a3)] = v[a0 * 4 + a3];
+  __syncwarp();
+  // ---- B: (a1, a2) slice at (k0, k3); axes 1 and 2
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = rbase[xoff(0, q >> 2, q & 3, 0)];
+  __syncwarp();
+#pragma unroll
+  for (int a2 = 0; a2 < 4; ++a2) fdct4<4>(v + a2, KC);  // axis 1
+#pragma unroll
+  for (int a1 = 0; a1 < 4; ++a1) fdct4<1>(v + a1 * 4, KC);  // axis 2
+  // v[k1*4 + k2] = C'[k0][k1][k2][k3]
+
+  // ---- block maximum (compare-select; non-finite -> N' = 0 or inf -> listed)
+  // signed winners, magnitudes compared through the |.| modifier (no
+  // instruction materialises |v|)
+  double m0 = 0.0, m1 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 16; q += 2) {
+    m0 = fabs(v[q]) > fabs(m0) ? v[q] : m0;
+    m1 = fabs(v[q + 1]) > fabs(m1) ? v[q + 1] : m1;
+  }
+  double m = fabs(m1) > fabs(m0) ? fabs(m1) : fabs(m0);
+#pragma unroll
+  for (int sft = 8; sft > 0; sft >>= 1) {
+    const double a = __shfl_xor_sync(0xffffffffu, m, sft);
+    m = a > m ? a : m;
+  }
+  const double mx = m * kUnscale;  // values carry the factor 16
+  const double n = round_to_kind<FK>(mx);
+  const BinCtx bc = bin_ctx<false>(n, 127.0, mx);
+  const double R16 = bc.R * kUnscale;
+  bool bad = !bc.fast || !(mx < 1.7976931348623157e308) ||
+             round_to_kind<FK>(mx * (1.0 - kDeltaRel)) != round_to_kind<FK>(mx * (1.0 + kDeltaRel));
+
+  // ---- bin the kept coefficients (24-bit fixed point, as bz_dct8.cu) into
+  // the warp's staging area at slot bs*K + rank (dropped ones: a scratch slot)
+  unsigned zmin = 0xffffffffu;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int fx = __double2loint(__fma_rn(v[q], R16, 1.5 * 268435456.0));
+    const unsigned y1 = (unsigned)fx + (1u << 23) + 1u;
+    zmin = min(zmin, rk[q] != ZS - bs * K ? (y1 & 0xffffffu) : 0xffffffffu);  // kept only
+    sbase[rk[q]] = (int8_t)(y1 >> 24);
+  }
+  bad = bad || zmin <= 2u;
+  const unsigned badmask = __ballot_sync(0xffffffffu, bad && valid);
+  if (valid && o == 0) {
+    store_kind<FK>(maxima, b, n);
+    if ((badmask >> (bs * 16)) & 0xffffu) list[atomicAdd(count, 1)] = (int32_t)b;
+  }
+  __syncwarp();
+  // ---- the warp tile's kept indices: one contiguous run of nvalid * K bytes
+  {
+    const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
+    const int nbytes = nv * K;
+    int8_t* dst = indices + b0 * (int64_t)K;
+    // staged contiguously: one word per lane (and a second) when aligned
+    if ((((uintptr_t)dst | (uintptr_t)nbytes) & 3) == 0) {
+      const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
+      uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+      for (int i = lane; i < nbytes / 4; i += 32) __stcs(d32 + i, s32[i]);
+    } else {
+      for (int e2 = lane; e2 < nbytes; e2 += 32) dst[e2] = stg[e2];
+    }
+  }
+}
+
 // --------------------------------------------------------------- compress --
 template <int FK>
 __global__ void __launch_bounds__(256, 3)
@@ -102,25 +210,20 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
   const int lane = t & 31, w = t >> 5;
   const int bs = lane >> 4, o = lane & 15;
   double* blk = reinterpret_cast<double*>(smem_raw) + (w * BPW + bs) * XS;
-  int8_t* stg = reinterpret_cast<int8_t*>(reinterpret_cast<double*>(smem_raw) + WPC * BPW * XS) +
-                w * BPW * SS;  // per-warp output staging, 2 x (256 + 16) bytes
   const int K = f.kept;
   const Dct4K KC = dct4_consts(p.H);
-  // this lane's 16 output positions (k0 = o>>2, k3 = o&3, k1, k2) -> staging
-  // slot: the warp tile's 2K indices are staged contiguously (block bs at
-  // bs*K); dropped coefficients go to the scratch slot ZS
-  constexpr int ZS = 2 * BS;
+  // rank (output slot within the block) of this lane's 16 coefficients
+  // (k0 = o>>2, k3 = o&3, k1, k2); -1 when the mask drops it
   const int k0 = o >> 2, k3 = o & 3;
   int16_t rk[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     const int r_ = f.full_mask ? (k0 * 64 + q * 4 + k3) : f.rank[k0 * 64 + q * 4 + k3];
-    rk[q] = (int16_t)(r_ >= 0 ? r_ : ZS - bs * K);
+    rk[q] = (int16_t)(r_ >= 0 ? r_ : 2 * BS - bs * K);  // dropped: the scratch slot
   }
   const int i1 = o >> 2, i2 = o & 3;
   double* wbase = blk + xoff(0, i1, i2, 0);  // phase A: (a0, a3) at immediates
   double* rbase = blk + xoff(k0, 0, 0, k3);  // phase B: (a1, a2) at immediates
-  int8_t* sbase = stg + bs * K;
   const int64_t s0 = f.stride[0], s1 = f.stride[1], s2 = f.stride[2];
   const int64_t nwt = (f.nblocks + BPW - 1) / BPW;
 
@@ -150,6 +253,9 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
     return full;
   };
   bool staged = prefetch(blockIdx.x * (int64_t)WPC + w);
+  int8_t* stg = reinterpret_cast<int8_t*>(reinterpret_cast<double*>(smem_raw) + WPC * BPW * XS) +
+                w * BPW * SS;  // per-warp output staging, 2 x (256 + 16) bytes
+  const Ctx4 cx{lane, bs, o, K, f.nblocks, KC, wbase, rbase, stg, stg + bs * K};
 
   for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += wstride) {
     const int64_t b = wt * BPW + bs;
@@ -186,77 +292,126 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
                                  ? (double)src[a0 * s0 + a3] : 0.0;
       }
     }
-#pragma unroll
-    for (int a3 = 0; a3 < 4; ++a3) fdct4<4>(v + a3, KC);  // axis 0
-#pragma unroll
-    for (int a0 = 0; a0 < 4; ++a0) fdct4<1>(v + a0 * 4, KC);  // axis 3
-#pragma unroll
-    for (int a0 = 0; a0 < 4; ++a0)
-#pragma unroll
-      for (int a3 = 0; a3 < 4; ++a3) wbase[xoff(a0, 0, 0, a3)] = v[a0 * 4 + a3];
-    __syncwarp();
-    // ---- B: (a1, a2) slice at (k0, k3); axes 1 and 2
-#pragma unroll
-    for (int q = 0; q < 16; ++q) v[q] = rbase[xoff(0, q >> 2, q & 3, 0)];
-    __syncwarp();
-#pragma unroll
-    for (int a2 = 0; a2 < 4; ++a2) fdct4<4>(v + a2, KC);  // axis 1
-#pragma unroll
-    for (int a1 = 0; a1 < 4; ++a1) fdct4<1>(v + a1 * 4, KC);  // axis 2
-    // v[k1*4 + k2] = C'[k0][k1][k2][k3]
+    dct4_compress_pair<FK>(v, rk, cx, wt * BPW, b, valid, maxima, indices, list, count);
+    __syncwarp();  // staging and exchange area reused by the next tile
+  }
+}
 
-    // ---- block maximum (compare-select; non-finite -> N' = 0 or inf -> listed)
-    double m0 = 0.0, m1 = 0.0;
-#pragma unroll
-    for (int q = 0; q < 16; q += 2) {
-      const double a = fabs(v[q]), c = fabs(v[q + 1]);
-      m0 = a > m0 ? a : m0;
-      m1 = c > m1 ? c : m1;
-    }
-    double m = m1 > m0 ? m1 : m0;
-#pragma unroll
-    for (int sft = 8; sft > 0; sft >>= 1) {
-      const double a = __shfl_xor_sync(0xffffffffu, m, sft);
-      m = a > m ? a : m;
-    }
-    const double mx = m * kUnscale;  // values carry the factor 16
-    const double n = round_to_kind<FK>(mx);
-    const BinCtx bc = bin_ctx<false>(n, 127.0, mx);
-    const double R16 = bc.R * kUnscale;
-    bool bad = !bc.fast || !(mx < 1.7976931348623157e308) ||
-               round_to_kind<FK>(mx * (1.0 - kDeltaRel)) != round_to_kind<FK>(mx * (1.0 + kDeltaRel));
+// ------------------------------------------------- compress, TMA tiles --
+// Tiles of 16 consecutive blocks along the last grid axis (a 4 x 4 x 4 x 64
+// f32 box = two TMA boxes of 4 x 4 x 4 x 32, 128-byte swizzled) stream
+// through a STAGES-deep ring of shared-memory buffers: warp 8 (one elected
+// lane) issues cp.async.bulk.tensor loads that complete on the stage's
+// `full` mbarrier; the 8 consumer warps (two blocks each, the lane layout
+// of k_dct4_compress) read their rows with conflict-free 16-byte loads,
+// release the stage on its `empty` mbarrier and run the shared pipeline.
+// No per-thread address arithmetic for the dense side: a block's linear
+// index is tile * 16 + j; out-of-range rows of partial blocks (axes 0-2)
+// arrive zero-filled by the TMA unit.
+namespace d4t {
+constexpr int NCW = 8;                  // consumer warps
+constexpr int NT = (NCW + 1) * 32;      // + producer warp
+constexpr int TB = 16;                  // blocks per tile
+constexpr int STAGES = 4;
+constexpr int BOX_BYTES = 8192;         // 4 x 4 x 4 x 32 f32
+constexpr int STAGE_BYTES = 2 * BOX_BYTES;
+constexpr size_t kSmem = 1024 + (size_t)STAGES * STAGE_BYTES + (size_t)NCW * 2 * d4::XS * 8 +
+                         (size_t)NCW * 2 * d4::SS + 2 * STAGES * 8;
+}  // namespace d4t
 
-    // ---- bin the kept coefficients (24-bit fixed point, as bz_dct8.cu)
-    unsigned zmin = 0xffffffffu;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int fx = __double2loint(__fma_rn(v[q], R16, 1.5 * 268435456.0));
-      const unsigned y1 = (unsigned)fx + (1u << 23) + 1u;
-      zmin = min(zmin, rk[q] != ZS - bs * K ? (y1 & 0xffffffu) : 0xffffffffu);  // kept only
-      sbase[rk[q]] = (int8_t)(y1 >> 24);
+template <int FK>
+__global__ void __launch_bounds__(d4t::NT, 2)
+k_dct4_compress_tma(const __grid_constant__ CUtensorMap xmap, const FastParams p,
+                    void* __restrict__ maxima, int8_t* __restrict__ indices,
+                    int32_t* __restrict__ list, int32_t* __restrict__ count) {
+  using namespace d4;
+  using namespace d4t;
+  const FastGeo& f = p.f;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // stages first, 1024-byte aligned (the 128-byte swizzle atom)
+  unsigned char* base = smem_raw + ((1024u - (tma::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t stage0 = tma::smem_u32(base);
+  double* xch = reinterpret_cast<double*>(base + STAGES * STAGE_BYTES);
+  int8_t* stg_all = reinterpret_cast<int8_t*>(xch + NCW * 2 * XS);
+  const uint32_t bar0 = tma::smem_u32(stg_all + NCW * 2 * SS);  // full[s] at bar0 + 8s
+  const uint32_t ebar0 = bar0 + 8 * STAGES;                      // empty[s]
+  const int t = threadIdx.x;
+  const int lane = t & 31, w = t >> 5;
+  const int64_t tpr = f.grid[3] / TB;  // tiles per row of blocks
+  const int64_t ntiles = f.nblocks / TB;
+  if (t == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tma::mbar_init(bar0 + 8 * s, 1);
+      tma::mbar_init(ebar0 + 8 * s, NCW);
     }
-    bad = bad || zmin <= 2u;
-    const unsigned badmask = __ballot_sync(0xffffffffu, bad && valid);
-    if (valid && o == 0) {
-      store_kind<FK>(maxima, b, n);
-      if ((badmask >> (bs * 16)) & 0xffffu) list[atomicAdd(count, 1)] = (int32_t)b;
-    }
-    __syncwarp();
-    // ---- the warp tile's kept indices: one contiguous run of nvalid * K bytes
-    {
-      const int64_t b0 = wt * BPW;
-      const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
-      const int nbytes = nv * K;
-      int8_t* dst = indices + b0 * (int64_t)K;
-      // staged contiguously: one word per lane (and a second) when aligned
-      if ((((uintptr_t)dst | (uintptr_t)nbytes) & 3) == 0) {
-        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
-        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-        for (int i = lane; i < nbytes / 4; i += 32) __stcs(d32 + i, s32[i]);
-      } else {
-        for (int e2 = lane; e2 < nbytes; e2 += 32) dst[e2] = stg[e2];
+    tma::fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (w == NCW) {  // ---------------------------------------------- producer
+    if (lane == 0) {
+      tma::prefetch_map(&xmap);
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+        if (it >= STAGES) tma::mbar_wait(ebar0 + 8 * s, ph ^ 1u);
+        tma::mbar_arrive_expect_tx(bar0 + 8 * s, STAGE_BYTES);
+        int64_t q = tile / tpr;
+        const int64_t r3 = tile - q * tpr;
+        const int64_t g2 = q % f.grid[2];
+        q /= f.grid[2];
+        const int64_t g1 = q % f.grid[1];
+        const int64_t g0 = q / f.grid[1];
+        const uint32_t dst = stage0 + s * STAGE_BYTES;
+        const int c3 = (int)(r3 * 64), c2 = (int)(g2 * 4), c1 = (int)(g1 * 4), c0 = (int)(g0 * 4);
+        tma::load_4d(dst, &xmap, bar0 + 8 * s, c3, c2, c1, c0);
+        tma::load_4d(dst + BOX_BYTES, &xmap, bar0 + 8 * s, c3 + 32, c2, c1, c0);
       }
     }
+    return;
+  }
+
+  // ---------------------------------------------------------------- consumers
+  const int bs = lane >> 4, o = lane & 15;
+  double* blk = xch + (w * 2 + bs) * XS;
+  int8_t* stg = stg_all + w * 2 * SS;
+  const int K = f.kept;
+  const Dct4K KC = dct4_consts(p.H);
+  const int k0 = o >> 2, k3 = o & 3;
+  int16_t rk[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int r_ = f.full_mask ? (k0 * 64 + q * 4 + k3) : f.rank[k0 * 64 + q * 4 + k3];
+    rk[q] = (int16_t)(r_ >= 0 ? r_ : 2 * BS - bs * K);  // dropped: the scratch slot
+  }
+  const int i1 = o >> 2, i2 = o & 3;
+  const Ctx4 cx{lane, bs, o, K, f.nblocks, KC, blk + xoff(0, i1, i2, 0), blk + xoff(k0, 0, 0, k3),
+                stg, stg + bs * K};
+  const int j = 2 * w + bs;  // block within the tile
+  // row r = a0*16 + o of box j/8, 16-byte chunk j%8 swizzled by r%8 = o%8
+  const uint32_t rd0 = (uint32_t)((j >> 3) * BOX_BYTES + o * 128 + (((j & 7) ^ (o & 7)) << 4));
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it % STAGES;
+    const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+    tma::mbar_wait(bar0 + 8 * s, ph);
+    const uint32_t src = stage0 + s * STAGE_BYTES + rd0;
+    float4 r[4];
+#pragma unroll
+    for (int a0 = 0; a0 < 4; ++a0) r[a0] = tma::lds128f(src + a0 * 16 * 128);
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(ebar0 + 8 * s);  // stage free for the producer
+    double v[16];
+#pragma unroll
+    for (int a0 = 0; a0 < 4; ++a0) {
+      v[a0 * 4 + 0] = (double)r[a0].x;
+      v[a0 * 4 + 1] = (double)r[a0].y;
+      v[a0 * 4 + 2] = (double)r[a0].z;
+      v[a0 * 4 + 3] = (double)r[a0].w;
+    }
+    const int64_t b0 = tile * TB + 2 * w;
+    dct4_compress_pair<FK>(v, rk, cx, b0, b0 + bs, true, maxima, indices, list, count);
     __syncwarp();  // staging and exchange area reused by the next tile
   }
 }
@@ -418,6 +573,23 @@ int launch_dct4_compress(const Geo& g, const void* x, void* maxima, void* indice
   int32_t* count = reinterpret_cast<int32_t*>(ws);
   int32_t* list = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(ws) + 256);
   if (cudaMemsetAsync(count, 0, sizeof(int32_t), s) != cudaSuccess) return check_launch("dct4 memset");
+  // TMA tiles: rows of 16 blocks along the last axis (dense, 16-byte strides)
+  CUtensorMap xmap;
+  const uint32_t box[4] = {4, 4, 4, 32};
+  if (!getenv("BZC_B200_NO_TMA") && g.grid[3] % d4t::TB == 0 && g.shape[3] == 4 * g.grid[3] &&
+      tma::encode_f32(&xmap, x, 4, g.shape, box)) {
+    auto kern = k_dct4_compress_tma<BZ_F32>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d4t::kSmem);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, d4t::NT, d4t::kSmem);
+    const int64_t ntiles = g.nblocks / d4t::TB;
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)kSMs * std::max(occ, 1));
+    kern<<<(int)grid, d4t::NT, d4t::kSmem, s>>>(xmap, p, maxima,
+                                                 reinterpret_cast<int8_t*>(indices), list, count);
+    if (int rc = check_launch("dct4_compress_tma")) return rc;
+    return launch_exact_compress(g, x, BZ_F32, maxima, indices, list, count,
+                                 std::min<int64_t>(g.nblocks, 4 * kSMs), nullptr, 0, s);
+  }
   const size_t smem = (size_t)WPC * BPW * XS * 8 + (size_t)WPC * BPW * SS + (size_t)4 * NT * 16;
   auto kern = k_dct4_compress<BZ_F32>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

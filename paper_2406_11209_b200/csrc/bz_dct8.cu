@@ -161,65 +161,74 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
   // staging slots ([row][thread], conflict-free) while this tile computes
   uint4* stage = reinterpret_cast<uint4*>(reinterpret_cast<double*>(smem_raw) + WPC * BPW * BS);
   const int64_t wstride = (int64_t)gridDim.x * WPC;
-  auto rows_src = [&](int64_t wt_, const TIn*& src, int64_t (&gc)[4]) -> bool {
+  // a warp tile's rows: coordinates are computed once per tile (when it is
+  // prefetched) and carried to the iteration that consumes it
+  struct Rows {
+    const TIn* src;
+    bool full;
+  };
+  auto coords_of = [&](int64_t wt_, int64_t& z0, int64_t& y, int64_t& x0) -> bool {
     const int64_t b_ = wt_ * BPW + bs;
     const bool ok = wt_ < nwt && b_ < f.nblocks;
-    gc[0] = gc[1] = gc[2] = gc[3] = 0;
+    int64_t gc[4] = {0, 0, 0, 0};
     if (ok) block_coords<3>(f, b_, gc);
-    const int64_t z0 = gc[0] * 8, y = gc[1] * 8 + hi, x0 = gc[2] * 8 + h * 4;
-    src = x + z0 * s0 + y * s1 + x0;
-    return sizeof(TIn) == 4 && f.vec_dense && ok && z0 + 8 <= f.shape[0] && y < f.shape[1] &&
-           x0 + 4 <= f.shape[2];
+    z0 = gc[0] * 8;
+    y = gc[1] * 8 + hi;
+    x0 = gc[2] * 8 + h * 4;
+    return ok;
   };
-  auto prefetch = [&](int64_t wt_) -> bool {
-    const TIn* src;
-    int64_t gc[4];
-    const bool full = rows_src(wt_, src, gc);
-    if (full) {
+  auto rows_of = [&](int64_t wt_) -> Rows {
+    int64_t z0, y, x0;
+    const bool ok = coords_of(wt_, z0, y, x0);
+    Rows r;
+    r.src = x + z0 * s0 + y * s1 + x0;
+    r.full = sizeof(TIn) == 4 && f.vec_dense && ok && z0 + 8 <= f.shape[0] && y < f.shape[1] &&
+             x0 + 4 <= f.shape[2];
+    return r;
+  };
+  auto prefetch = [&](const Rows& r) {
+    if (r.full) {
 #pragma unroll
-      for (int z = 0; z < 8; ++z) cp_async16(stage + z * NT + t, src + z * s0);
+      for (int z = 0; z < 8; ++z) cp_async16(stage + z * NT + t, r.src + z * s0);
     }
     cp_async_commit();
-    return full;
   };
-  bool staged = prefetch(blockIdx.x * (int64_t)WPC + w);
+  Rows cur = rows_of(blockIdx.x * (int64_t)WPC + w);
+  prefetch(cur);
 
   for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += wstride) {
     const int64_t b = wt * BPW + bs;
     const bool valid = b < f.nblocks;
+    const Rows nxt = rows_of(wt + wstride);
 
     // ---- A: thread (y = hi, x half h): rows z = 0..7 of 4 x, axis 0
     double v[32];
-    {
-      const TIn* src;
-      int64_t gc[4];
-      const bool full = rows_src(wt, src, gc);
-      const int64_t z0 = gc[0] * 8, y = gc[1] * 8 + hi, x0 = gc[2] * 8 + h * 4;
-      if (staged) {
-        cp_async_wait_all();
-        uint4 r[8];
+    if (cur.full) {
+      cp_async_wait_all();
+      uint4 r[8];
 #pragma unroll
-        for (int z = 0; z < 8; ++z) r[z] = stage[z * NT + t];
-        staged = prefetch(wt + wstride);  // own slots, already read
+      for (int z = 0; z < 8; ++z) r[z] = stage[z * NT + t];
+      prefetch(nxt);  // own slots, already read
 #pragma unroll
-        for (int z = 0; z < 8; ++z) {
-          v[z * 4 + 0] = (double)__uint_as_float(r[z].x);
-          v[z * 4 + 1] = (double)__uint_as_float(r[z].y);
-          v[z * 4 + 2] = (double)__uint_as_float(r[z].z);
-          v[z * 4 + 3] = (double)__uint_as_float(r[z].w);
-        }
-      } else {
-        (void)full;
-        staged = prefetch(wt + wstride);
-        const bool okyx = valid && y < f.shape[1];
-#pragma unroll
-        for (int z = 0; z < 8; ++z)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            v[z * 4 + j] = (okyx && z0 + z < f.shape[0] && x0 + j < f.shape[2])
-                               ? widen(src[z * s0 + j]) : 0.0;
+      for (int z = 0; z < 8; ++z) {
+        v[z * 4 + 0] = (double)__uint_as_float(r[z].x);
+        v[z * 4 + 1] = (double)__uint_as_float(r[z].y);
+        v[z * 4 + 2] = (double)__uint_as_float(r[z].z);
+        v[z * 4 + 3] = (double)__uint_as_float(r[z].w);
       }
+    } else {  // partial block or another input kind: predicated loads
+      prefetch(nxt);
+      int64_t z0, y, x0;
+      coords_of(wt, z0, y, x0);
+      const bool okyx = valid && y < f.shape[1];
+#pragma unroll
+      for (int z = 0; z < 8; ++z)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          v[z * 4 + j] = (okyx && z0 + z < f.shape[0] && x0 + j < f.shape[2])
+                             ? widen(cur.src[z * s0 + j]) : 0.0;
     }
+    cur = nxt;
 #pragma unroll
     for (int j = 0; j < 4; ++j) fdct8<4>(v + j, KC);
 #pragma unroll
@@ -265,14 +274,13 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
     // compares false and is dropped; non-finite inputs make every coefficient
     // non-finite -- all H entries are nonzero -- so such blocks end with
     // N' = 0 or inf and are flagged below)
+    // (the chains carry the signed winner and compare magnitudes through the
+    // |.| operand modifier, so no instruction materialises |c|)
     double m4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains (latency)
 #pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const double a = fabs(c[q]);
-      m4[q & 3] = a > m4[q & 3] ? a : m4[q & 3];
-    }
-    double m = m4[0] > m4[1] ? m4[0] : m4[1];
-    const double m23 = m4[2] > m4[3] ? m4[2] : m4[3];
+    for (int q = 0; q < 32; ++q) m4[q & 3] = fabs(c[q]) > fabs(m4[q & 3]) ? c[q] : m4[q & 3];
+    double m = fabs(m4[0]) > fabs(m4[1]) ? fabs(m4[0]) : fabs(m4[1]);
+    const double m23 = fabs(m4[2]) > fabs(m4[3]) ? fabs(m4[2]) : fabs(m4[3]);
     m = m23 > m ? m23 : m;
 #pragma unroll
     for (int sft = 8; sft > 0; sft >>= 1) {

@@ -75,25 +75,36 @@ def run(name):
     cb = bz.compress(y, s)
     rows = []
 
+    only = [o for o in os.environ.get("QB_OPS", "").split(",") if o]
+
+    def timeit_(fn, reps=10, warm=3):
+        return timeit(fn, reps, warm)
+
+    def rec_(op, ms_thunk_or_ms, alg_bytes, in_bytes=inb):
+        if only and op not in only:
+            return
+        rec(op, ms_thunk_or_ms() if callable(ms_thunk_or_ms) else ms_thunk_or_ms, alg_bytes,
+            in_bytes)
+
     def rec(op, ms, alg_bytes, in_bytes=inb):
         rows.append((op, ms, in_bytes / ms / 1e6, alg_bytes / ms / 1e6, alg_bytes / ms / 1e6 / peak))
 
-    rec("compress", timeit(lambda: bz.compress(x, s)), inb + comp_bytes)
-    rec("decompress_f64", timeit(lambda: bz.decompress(ca)), comp_bytes + n * 8)
-    rec("decompress_fk", timeit(lambda: bz.decompress(ca, kind)), comp_bytes + n * kind.itemsize)
-    rec("l2_record", timeit(lambda: bz.ops.moments_record(ca, dc_only=2)), comp_bytes)
-    rec("dot_record", timeit(lambda: bz.ops.moments_record(ca, cb, dc_only=2)), 2 * comp_bytes, 2 * inb)
-    rec("add", timeit(lambda: bz.add(ca, cb)), 3 * comp_bytes, 2 * inb)
-    rec("negate", timeit(lambda: bz.negate(ca)), 2 * B * K * s.index_kind.itemsize)
-    rec("l2_norm(api)", timeit(lambda: bz.l2_norm(ca)), comp_bytes)
-    rec("mean(api)", timeit(lambda: bz.mean(ca)), B * (s.index_kind.itemsize + kind.itemsize))
+    rec_("compress", lambda: timeit(lambda: bz.compress(x, s)), inb + comp_bytes)
+    rec_("decompress_f64", lambda: timeit(lambda: bz.decompress(ca)), comp_bytes + n * 8)
+    rec_("decompress_fk", lambda: timeit(lambda: bz.decompress(ca, kind)), comp_bytes + n * kind.itemsize)
+    rec_("l2_record", lambda: timeit(lambda: bz.ops.moments_record(ca, dc_only=2)), comp_bytes)
+    rec_("dot_record", lambda: timeit(lambda: bz.ops.moments_record(ca, cb, dc_only=2)), 2 * comp_bytes, 2 * inb)
+    rec_("add", lambda: timeit(lambda: bz.add(ca, cb)), 3 * comp_bytes, 2 * inb)
+    rec_("negate", lambda: timeit(lambda: bz.negate(ca)), 2 * B * K * s.index_kind.itemsize)
+    rec_("l2_norm(api)", lambda: timeit(lambda: bz.l2_norm(ca)), comp_bytes)
+    rec_("mean(api)", lambda: timeit(lambda: bz.mean(ca)), B * (s.index_kind.itemsize + kind.itemsize))
     if s.mask.keeps_first:
-        rec("cov(api)", timeit(lambda: bz.covariance(ca, cb)), 2 * comp_bytes, 2 * inb)
-        rec("ssim(api)", timeit(lambda: bz.ssim(ca, cb)), 2 * comp_bytes, 2 * inb)
-        rec("subtract_l2", timeit(lambda: bz.subtract_l2(cb, ca)), 2 * comp_bytes, 2 * inb)
-        rec("wasserstein", timeit(lambda: bz.approx_wasserstein(ca, cb), reps=3, warm=1),
+        rec_("cov(api)", lambda: timeit(lambda: bz.covariance(ca, cb)), 2 * comp_bytes, 2 * inb)
+        rec_("ssim(api)", lambda: timeit(lambda: bz.ssim(ca, cb)), 2 * comp_bytes, 2 * inb)
+        rec_("subtract_l2", lambda: timeit(lambda: bz.subtract_l2(cb, ca)), 2 * comp_bytes, 2 * inb)
+        rec_("wasserstein", lambda: timeit(lambda: bz.approx_wasserstein(ca, cb), reps=3, warm=1),
             2 * B * (s.index_kind.itemsize + kind.itemsize))
-    rec("serialize_dev", timeit(lambda: bz.serialize_to_device(ca)), 2 * comp_bytes)
+    rec_("serialize_dev", lambda: timeit(lambda: bz.serialize_to_device(ca)), 2 * comp_bytes)
     print(f"== {name} shape={shape} block={block} {fk}/{ik} K={K} fast={bz.is_fast_path(s, shape)}")
     for op, ms, g_in, g_alg, frac in rows:
         print(f"  {op:16s} {ms*1e3:9.1f} us  in {g_in:8.0f} GB/s  alg {g_alg:7.0f} GB/s  frac {frac:.3f}")
