@@ -6,6 +6,7 @@
 #include "bz_fast.cuh"
 #include "bz_kernels.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace bz {
@@ -529,6 +530,19 @@ k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
                         (MODE != 0 || (nb >= 0x1p-900 && nb <= 0x1p+900));
       double c[CPL];
       unsigned long long key = 0;
+      // narrow maxima (F32): F * N is exact and fl(F N / r) = fma(F, t_hi,
+      // F * t_lo) with t = N / r split in two (bz_add8.cu has the proof)
+      constexpr bool NARROW = FK != BZ_F64;
+      double tha = 0.0, tla = 0.0, thb = 0.0, tlb = 0.0;
+      if (NARROW) {
+        tha = div_const(na, r, rinv);
+        tla = __fma_rn(-tha, r, na) * rinv;
+        if (MODE == 0) {
+          thb = div_const(nb, r, rinv);
+          tlb = __fma_rn(-thb, r, nb) * rinv;
+          if (subtract) { thb = -thb; tlb = -tlb; }
+        }
+      }
       auto coeffs = [&](auto safe_tag) {
         constexpr bool SAFE = decltype(safe_tag)::value;
         double mxd = 0.0;
@@ -538,7 +552,18 @@ k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
           double cc = 0.0;
           if (k < kept) {
             const int fa = (int)pa[k];
-            if constexpr (SAFE) {
+            if constexpr (SAFE && NARROW) {
+              const double fad = (double)fa;
+              cc = __fma_rn(fad, tha, fad * tla);
+              if (MODE == 0) {
+                const double fbd = (double)(int)pb[k];
+                cc = __dadd_rn(cc, __fma_rn(fbd, thb, fbd * tlb));
+              } else if (k == 0) {
+                cc = __dadd_rn(cc, shift);
+              }
+              const double a = fabs(cc);
+              mxd = a > mxd ? a : mxd;
+            } else if constexpr (SAFE) {
               const double xa = div_const(fn_product(fa, sca), r, rinv);
               if (MODE == 0) {
                 const int fb = subtract ? -(int)pb[k] : (int)pb[k];
@@ -614,6 +639,10 @@ template <typename IT>
 static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                         const void* b_max, const void* b_idx, int subtract, double shift,
                         int mode, void* out_max, void* out_idx, cudaStream_t s) {
+  // int8 indices with float32 maxima, whole 16-byte chunks: bz_add8.cu
+  if (sizeof(IT) == 1 && add8_supported(ga, gb, mode, a_idx, b_idx, out_idx) &&
+      !getenv("BZC_B200_NO_ADD8"))
+    return launch_add8(ga, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s);
   constexpr int V = 16 / sizeof(IT);
   const int kept = ga.kept;
   const int vecs = (kept + V - 1) / V;  // chunks per block

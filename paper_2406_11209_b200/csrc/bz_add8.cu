@@ -1,0 +1,232 @@
+// bz_add8.cu -- add / subtract / add_scalar for int8 indices with float32
+// maxima (the C3 / C4 chain, ops.py:178-215), bit-exact with the reference.
+//
+// The reference computes every coefficient as fl(fl(F * N) / r) (codec.py:
+// 337-350), sums the two operands, takes the block maximum and rebins.  For
+// int8 F and a float32 N the product F * N is exact (8 + 24 bits), so
+// fl(F * N / r) = RN(F * t) with t = N / r.  With t_hi = RN(t) and
+// t_lo = RN(t - t_hi) (the remainder is exact by FMA) the kernel evaluates
+//     x = fma(F, t_hi, F * t_lo)
+// -- two FP64 operations instead of a product and a correctly rounded
+// division.  Exactness: F * t_hi + RN(F * t_lo) differs from F * t by less
+// than 2^-98 |F t|, while F * t = F N / 127 is either representable or sits
+// at least 2^-8 ulp away from every rounding boundary (its binary expansion
+// beyond the significand is j/127 of an ulp, 2 having order 7 modulo 127,
+// and a midpoint would need j/127 = 1/2).  So x equals the reference's
+// fl(fl(F N) / r) bit for bit.  Subtract negates t_hi and t_lo (exact).
+//
+// Rebinning uses the 24-bit fixed point of bz_dct8.cu (one FMA per
+// coefficient); a block whose maxima are tiny / huge / zero / non-finite,
+// whose stored maximum could round differently, or with a coefficient
+// within one fixed-point unit of a rounding half, is recomputed by the
+// group with the exact IEEE path (codec.py:253-278) right away.
+#include "bz_common.cuh"
+#include "bz_fast.cuh"
+#include "bz_kernels.cuh"
+
+namespace bz {
+
+namespace {
+
+// exact per-block path (rare): IEEE product, division, NaN-propagating
+// maximum and exact binning, GS lanes of the group cooperating
+template <int GS, int MODE>
+__device__ __noinline__ void add8_block_exact(int64_t b, int kept, int sub, unsigned gmask,
+                                              const float* __restrict__ a_max,
+                                              const int8_t* __restrict__ a_idx,
+                                              const float* __restrict__ b_max,
+                                              const int8_t* __restrict__ b_idx, int subtract,
+                                              double shift, float* __restrict__ out_max,
+                                              int8_t* __restrict__ out_idx) {
+  const double r = 127.0;
+  const int64_t base = b * (int64_t)kept;
+  const double na = (double)a_max[b];
+  const double nb = MODE == 0 ? (double)b_max[b] : 0.0;
+  auto coeff = [&](int k) -> double {
+    const double xa = __ddiv_rn(__dmul_rn((double)a_idx[base + k], na), r);
+    if (MODE == 0) {
+      const double fb = subtract ? -(double)b_idx[base + k] : (double)b_idx[base + k];
+      return __dadd_rn(xa, __ddiv_rn(__dmul_rn(fb, nb), r));
+    }
+    return k == 0 ? __dadd_rn(xa, shift) : xa;
+  };
+  double m = 0.0;
+  for (int k = sub; k < kept; k += GS) m = nanmax_abs(m, coeff(k));
+#pragma unroll
+  for (int o = GS / 2; o > 0; o >>= 1) {
+    const double t = __shfl_xor_sync(gmask, m, o, GS);
+    m = (isnan(t) || isnan(m)) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(m, t);
+  }
+  const double n = round_to_kind<BZ_F32>(m);
+  if (sub == 0) out_max[b] = (float)n;
+  for (int k = sub; k < kept; k += GS) out_idx[base + k] = (int8_t)bin_exact(coeff(k), n, r, r);
+}
+
+}  // namespace
+
+// GS lanes per block, NCH 16-byte chunks (16 indices) per lane; the next
+// block's chunks and maxima are loaded while the current block computes.
+template <int GS, int NCH, int MODE>
+__global__ void __launch_bounds__(256, NCH == 1 ? 3 : 2)
+k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
+       const int8_t* __restrict__ a_idx, const float* __restrict__ b_max,
+       const int8_t* __restrict__ b_idx, int subtract, double shift,
+       float* __restrict__ out_max, int8_t* __restrict__ out_idx) {
+  constexpr double r = 127.0, rinv = 1.0 / 127.0;
+  constexpr int L = NCH * 16;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % GS;
+  const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1) << (lane - sub));
+  const int64_t group = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GS;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / GS;
+
+  uint4 pa[NCH], pb[NCH];
+  float pna = 0.f, pnb = 0.f;
+  auto fetch = [&](int64_t b) {
+    if (b < nblocks) {
+      const int64_t base = b * (int64_t)kept;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int k0 = (ch * GS + sub) * 16;
+        pa[ch] = k0 < kept ? __ldcs(reinterpret_cast<const uint4*>(a_idx + base + k0))
+                           : make_uint4(0, 0, 0, 0);
+        pb[ch] = (MODE == 0 && k0 < kept)
+                     ? __ldcs(reinterpret_cast<const uint4*>(b_idx + base + k0))
+                     : make_uint4(0, 0, 0, 0);
+      }
+      pna = __ldcs(a_max + b);
+      pnb = MODE == 0 ? __ldcs(b_max + b) : 0.f;
+    }
+  };
+  fetch(group);
+
+  for (int64_t b = group; b < nblocks; b += ngroups) {
+    const int64_t base = b * (int64_t)kept;
+    uint4 ca[NCH], cb[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      ca[ch] = pa[ch];
+      cb[ch] = pb[ch];
+    }
+    const double na = (double)pna, nb = (double)pnb;
+    fetch(b + ngroups);
+
+    bool safe = na >= 0x1p-900 && na <= 0x1p+900;
+    if (MODE == 0) safe = safe && nb >= 0x1p-900 && nb <= 0x1p+900;
+    // t = N / r as t_hi + t_lo (t_hi correctly rounded, remainder exact by FMA)
+    const double tha = div_const(na, r, rinv);
+    const double tla = __fma_rn(-tha, r, na) * rinv;
+    double thb = 0.0, tlb = 0.0;
+    if (MODE == 0) {
+      thb = div_const(nb, r, rinv);
+      tlb = __fma_rn(-thb, r, nb) * rinv;
+      if (subtract) { thb = -thb; tlb = -tlb; }
+    }
+    double c[L];
+    double m4[4];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      const uint32_t wa[4] = {ca[ch].x, ca[ch].y, ca[ch].z, ca[ch].w};
+      const uint32_t wb[4] = {cb[ch].x, cb[ch].y, cb[ch].z, cb[ch].w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const double fa = (double)(int)(int8_t)(wa[e >> 2] >> (8 * (e & 3)));
+        double cc = __fma_rn(fa, tha, fa * tla);
+        if (MODE == 0) {
+          const double fb = (double)(int)(int8_t)(wb[e >> 2] >> (8 * (e & 3)));
+          cc = __dadd_rn(cc, __fma_rn(fb, thb, fb * tlb));
+        } else if (ch == 0 && e == 0) {
+          if (sub == 0) cc = __dadd_rn(cc, shift);
+        }
+        c[ch * 16 + e] = cc;
+        // chunks past `kept` hold zeros: they cannot raise the maximum; the
+        // chains start from real elements (from 0.0 the compiler assumes a
+        // non-negative running value and drops the |.| -- see bz_dct8.cu)
+        if (ch == 0 && e < 4) m4[e] = cc;
+        else m4[e & 3] = fabs(cc) > fabs(m4[e & 3]) ? cc : m4[e & 3];
+      }
+    }
+    double m = fabs(m4[0]) > fabs(m4[1]) ? fabs(m4[0]) : fabs(m4[1]);
+    const double m23 = fabs(m4[2]) > fabs(m4[3]) ? fabs(m4[2]) : fabs(m4[3]);
+    m = m23 > m ? m23 : m;
+#pragma unroll
+    for (int o = GS / 2; o > 0; o >>= 1) {
+      const double t = __shfl_xor_sync(gmask, m, o, GS);
+      m = t > m ? t : m;
+    }
+    const double n = round_to_kind<BZ_F32>(m);
+    const BinCtx bc = bin_ctx<false>(n, r, m);
+    // 24-bit fixed point (bz_dct8.cu): index = top byte of y unless the
+    // fraction is within one unit of one half
+    unsigned z4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+    uint4 ov[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      unsigned y[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int fx = __double2loint(__fma_rn(c[ch * 16 + e], bc.R, 1.5 * 268435456.0));
+        y[e] = (unsigned)fx + (1u << 23) + 1u;
+        z4[e & 3] = min(z4[e & 3], y[e] & 0xffffffu);
+      }
+      unsigned wd[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        wd[k] = __byte_perm(__byte_perm(y[4 * k], y[4 * k + 1], 0x0073),
+                            __byte_perm(y[4 * k + 2], y[4 * k + 3], 0x0073), 0x5410);
+      ov[ch] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    }
+    const bool near = min(min(z4[0], z4[1]), min(z4[2], z4[3])) <= 2u;
+    const bool bad = !safe || !bc.fast || !(m < 1.7976931348623157e308);
+    const bool any_bad = (__ballot_sync(gmask, near || bad) & gmask) != 0u;
+    if (!any_bad) {
+      if (sub == 0) out_max[b] = (float)n;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int k0 = (ch * GS + sub) * 16;
+        if (k0 < kept) __stcs(reinterpret_cast<uint4*>(out_idx + base + k0), ov[ch]);
+      }
+    } else {  // group-uniform: the exact path for this block
+      add8_block_exact<GS, MODE>(b, kept, sub, gmask, a_max, a_idx, b_max, b_idx, subtract, shift,
+                                 out_max, out_idx);
+    }
+  }
+}
+
+bool add8_supported(const Geo& ga, const Geo& gb, int mode, const void* a_idx, const void* b_idx,
+                    const void* out_idx) {
+  if (ga.index_kind != BZ_I8 || ga.float_kind != BZ_F32) return false;
+  if (mode == 0 && gb.float_kind != BZ_F32) return false;
+  if (ga.kept < 16 || ga.kept % 16 || ga.kept > 32 * 16 * 2) return false;
+  const uintptr_t al = (uintptr_t)a_idx | (uintptr_t)out_idx | (mode == 0 ? (uintptr_t)b_idx : 0);
+  return (al & 15) == 0;
+}
+
+int launch_add8(const Geo& ga, const void* a_max, const void* a_idx, const void* b_max,
+                const void* b_idx, int subtract, double shift, int mode, void* out_max,
+                void* out_idx, cudaStream_t s) {
+  const int vecs = ga.kept / 16;
+  int GS = 1;
+  while (GS < 32 && GS < vecs) GS <<= 1;
+  const int NCH = (vecs + GS - 1) / GS;  // 1 or 2
+  const int grid = grid_for(ga.nblocks * GS, 256, 3);
+#define BZ_A8(G, N, M)                                                                        \
+  k_add8<G, N, M><<<grid, 256, 0, s>>>(ga.nblocks, ga.kept, (const float*)a_max,              \
+                                       (const int8_t*)a_idx, (const float*)b_max,             \
+                                       (const int8_t*)b_idx, subtract, shift, (float*)out_max, \
+                                       (int8_t*)out_idx)
+#define BZ_A8M(G, N) \
+  do { if (mode == 0) BZ_A8(G, N, 0); else BZ_A8(G, N, 1); } while (0)
+#define BZ_A8G(G)             \
+  case G:                     \
+    if (NCH == 1) BZ_A8M(G, 1); \
+    else BZ_A8M(G, 2);        \
+    break;
+  switch (GS) { BZ_A8G(1) BZ_A8G(2) BZ_A8G(4) BZ_A8G(8) BZ_A8G(16) BZ_A8G(32) }
+#undef BZ_A8G
+#undef BZ_A8M
+#undef BZ_A8
+  return check_launch("add8");
+}
+
+}  // namespace bz

@@ -145,9 +145,10 @@ __device__ __forceinline__ void dct4_compress_pair(double (&v)[16], const int16_
   // ---- block maximum (compare-select; non-finite -> N' = 0 or inf -> listed)
   // signed winners, magnitudes compared through the |.| modifier (no
   // instruction materialises |v|)
-  double m0 = 0.0, m1 = 0.0;
+  // (chains start from real elements, not 0.0: see bz_dct8.cu)
+  double m0 = v[0], m1 = v[1];
 #pragma unroll
-  for (int q = 0; q < 16; q += 2) {
+  for (int q = 2; q < 16; q += 2) {
     m0 = fabs(v[q]) > fabs(m0) ? v[q] : m0;
     m1 = fabs(v[q + 1]) > fabs(m1) ? v[q + 1] : m1;
   }

@@ -276,9 +276,11 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
     // N' = 0 or inf and are flagged below)
     // (the chains carry the signed winner and compare magnitudes through the
     // |.| operand modifier, so no instruction materialises |c|)
-    double m4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains (latency)
+    // (chains start from real elements: starting from 0.0 lets the compiler
+    // assume a non-negative running value and drop the |.| -- wrong results)
+    double m4[4] = {c[0], c[1], c[2], c[3]};  // four independent chains (latency)
 #pragma unroll
-    for (int q = 0; q < 32; ++q) m4[q & 3] = fabs(c[q]) > fabs(m4[q & 3]) ? c[q] : m4[q & 3];
+    for (int q = 4; q < 32; ++q) m4[q & 3] = fabs(c[q]) > fabs(m4[q & 3]) ? c[q] : m4[q & 3];
     double m = fabs(m4[0]) > fabs(m4[1]) ? fabs(m4[0]) : fabs(m4[1]);
     const double m23 = fabs(m4[2]) > fabs(m4[3]) ? fabs(m4[2]) : fabs(m4[3]);
     m = m23 > m ? m23 : m;

@@ -85,6 +85,11 @@ int launch_stream_unpack(const void* in, int64_t in_words, int64_t bit_offset, v
 int launch_negate(int ik, const void* in, void* out, int64_t n, cudaStream_t s);
 int launch_mul_scalar(const Geo& g, const void* maxima, const void* indices, double x,
                       void* maxima_out, void* indices_out, cudaStream_t s);
+bool add8_supported(const Geo& ga, const Geo& gb, int mode, const void* a_idx, const void* b_idx,
+                    const void* out_idx);
+int launch_add8(const Geo& ga, const void* a_max, const void* a_idx, const void* b_max,
+                const void* b_idx, int subtract, double shift, int mode, void* out_max,
+                void* out_idx, cudaStream_t s);
 int launch_add(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                const void* b_max, const void* b_idx, int subtract, double shift, int mode,
                void* out_max, void* out_idx, cudaStream_t s);

@@ -385,6 +385,12 @@ def test_dct4_flagged_blocks(bz, monkeypatch, mask):
     ((16, 16), "f64", "i8", 200),        # 32 lanes per block
     ((8, 8, 16), "f32", "i16", 300),     # 32 lanes x 16 (600-byte blocks)
     ((8, 8, 16), "f64", "i8", 700),      # > 512 kept: two-pass staged add
+    # whole 16-byte chunks, int8 + float32 maxima: the t_hi/t_lo kernel (bz_add8.cu)
+    ((8, 8, 8), "f32", "i8", 512),       # C3 / C4: 32 lanes per block
+    ((8, 8, 8), "f32", "i8", 256),       # 16 lanes per block
+    ((4, 4, 4, 4), "f32", "i8", 64),     # 4 lanes per block
+    ((8, 8), "f32", "i8", 16),           # one lane per block
+    ((16, 16, 8), "f32", "i8", 1024),    # two chunks per lane
 ])
 def test_elementwise_unaligned_blocks(bz, block, fk, ik, keep):
     """add / subtract / add_scalar / negate on blocks whose kept indices are
@@ -423,3 +429,26 @@ def test_elementwise_unaligned_blocks(bz, block, fk, ik, keep):
     for p_, q_, rp, rq in ((a, b, ra, rb), (b, a, rb, ra)):
         got, want = bz.subtract_l2(p_, q_), o.l2_norm(o.subtract(rp, rq))
         assert math.isclose(got, want, rel_tol=1e-12), (got, want)
+
+
+@pytest.mark.parametrize("shape,block,mask", [
+    ((64, 64, 64), (8, 8, 8), None),
+    ((16, 16, 16, 16), (4, 4, 4, 4), "lowpass"),
+    ((16, 16, 16, 16), (4, 4, 4, 4), None),
+])
+def test_negative_dominant_coefficients(bz, shape, block, mask):
+    """Blocks whose largest-magnitude coefficient is negative and sits first in
+    a lane's maximum chain (the DC term of negative, nearly constant blocks),
+    and differences of nearly equal arrays (cancellation: a small negative DC
+    dominates).  Guards the compare-select maximum in the factored compress
+    kernels and the add kernels."""
+    rng = np.random.default_rng(99)
+    bits = _lowpass(block, 4) if mask == "lowpass" else None
+    x = -(1.0 + 0.01 * rng.normal(size=shape))
+    y = x + 1e-4 * rng.normal(size=shape) + 3e-3
+    ca, ra, _ = parity(bz, x, block, "f32", "i8", mask_bits=bits)
+    cb, rb, _ = parity(bz, y, block, "f32", "i8", mask_bits=bits)
+    for got, want in ((bz.subtract(ca, cb), o.subtract(ra, rb)), (bz.add(ca, cb), o.add(ra, rb)),
+                      (bz.subtract(cb, ca), o.subtract(rb, ra))):
+        assert np.array_equal(got.maxima_f64().cpu().numpy(), want.maxima)
+        assert np.array_equal(got.indices.cpu().numpy(), want.indices)

@@ -196,3 +196,25 @@ def test_c4_full_size_reductions_vs_chunked_oracle(bz):
         assert math.isclose(got[k], want[k], rel_tol=1e-9, abs_tol=1e-15), (k, got[k], want[k])
     # the fused covariance really sees a correlated pair
     assert 0.5 < got["cosine"] < 0.9
+
+
+def test_c3_slab_add_chain_bit_exact(bz):
+    """add / subtract / add_scalar / mul_scalar of two GPU-compressed C3 slabs
+    vs the oracle on the same compressed data, chunk by chunk (ops.py:178-223)."""
+    s = _settings(bz, (8, 8, 8), "f32", "i8")
+    a = bz.compress(_fill(bz, (64, 1024, 1024), bz.FloatKind.F32, 61), s)
+    b = bz.compress(_fill(bz, (64, 1024, 1024), bz.FloatKind.F32, 62), s)
+    os_ = o.Settings((8, 8, 8), "f32", "i8")
+    results = [("add", bz.add(a, b)), ("sub", bz.subtract(a, b)),
+               ("adds", bz.add_scalar(a, 0.375)), ("chain", bz.mul_scalar(bz.add(a, b), 0.5))]
+    for g0 in range(0, 8, 2):
+        sl = slice(g0, g0 + 2)
+        shp = (16, 1024, 1024)
+        ra = o.Compressed(shp, os_, a.maxima_f64()[sl].cpu().numpy(), a.indices[sl].cpu().numpy())
+        rb = o.Compressed(shp, os_, b.maxima_f64()[sl].cpu().numpy(), b.indices[sl].cpu().numpy())
+        want = {"add": o.add(ra, rb), "sub": o.subtract(ra, rb), "adds": o.add_scalar(ra, 0.375)}
+        want["chain"] = o.mul_scalar(want["add"], 0.5)
+        for name, got in results:
+            w = want[name]
+            assert np.array_equal(got.maxima_f64()[sl].cpu().numpy(), w.maxima), (name, g0)
+            assert np.array_equal(got.indices[sl].cpu().numpy(), w.indices), (name, g0)
