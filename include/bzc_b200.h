@@ -83,13 +83,25 @@ const char* bz_last_error(void);
 long long bz_launch_count(void);
 /* Which compress kernel a layout dispatches to: 1 = fused fast path, 0 = generic. */
 int bz_fast_path(const bz_layout* L);
+/* Wait for `stream` (the one host synchronisation of a scalar reduction);
+ * BZ_E_CUDA on an asynchronous launch error.                                */
+int bz_stream_sync(void* stream);
+/* Wait until a reduction record in pinned host memory is complete: spins on
+ * its completion flag record[BZ_RECORD_DOUBLES-1] (the caller zeroes it
+ * before the launch; the kernel stores 1.0 last), checking the stream every
+ * ~1k polls so a failed launch returns BZ_E_CUDA instead of hanging.       */
+int bz_wait_record(const double* record, void* stream);
 
 /* ---- codec: compress / decompress (codec.py:321-334, 364-384) ---------- */
 /* x: dense row-major values of kind x_kind (already exactly representable in
- * it).  Outputs: maxima[grid] in float_kind storage, indices[grid][K].       */
+ * it).  Outputs: maxima[grid] in float_kind storage, indices[grid][K].
+ * dc (optional, may be NULL; ignored when the mask drops the first
+ * coefficient): the DC plane dc[b] = indices[b][0], contiguous, in the index
+ * kind -- what mean reads (bz_moments_dc) instead of a stride-K gather.     */
 size_t bz_compress_workspace(const bz_layout* L);
 int bz_compress(const bz_layout* L, const void* x, int x_kind, void* maxima,
-                void* indices, void* workspace, size_t workspace_bytes, void* stream);
+                void* indices, void* dc, void* workspace, size_t workspace_bytes,
+                void* stream);
 
 /* out: dense row-major values of out_kind (BZ_F64 = reference semantics,
  * codec.py:367; narrower kinds round the f64 result once).                  */
@@ -102,18 +114,23 @@ int bz_decompress(const bz_layout* L, const void* maxima, const void* indices,
 /* negate: out = -in over `count` indices (ops.py:195-197). */
 int bz_negate(int index_kind, const void* in, void* out, int64_t count, void* stream);
 /* mul_scalar: maxima_out = RN_kind(maxima * |x|); indices_out = indices * sign(x)
- * (ops.py:218-223).  indices_out may be NULL when x > 0 (indices aliased).   */
-int bz_mul_scalar(const bz_layout* L, const void* maxima, const void* indices, double x,
-                  void* maxima_out, void* indices_out, void* stream);
+ * (ops.py:218-223).  indices_out may be NULL when x > 0 (indices aliased).
+ * dc / dc_out (optional DC planes): dc_out = dc * sign(x) when x <= 0 or NaN
+ * (NULL when x > 0: the plane is aliased like the indices).                  */
+int bz_mul_scalar(const bz_layout* L, const void* maxima, const void* indices, const void* dc,
+                  double x, void* maxima_out, void* indices_out, void* dc_out, void* stream);
 /* add / subtract with rebinning under La's kinds (ops.py:178-204; subtract =
  * add(a, negate(b)), cli.py:242).  Bit-exact with the reference.            */
+/* out_dc (optional): the result's DC plane (see bz_compress).             */
 int bz_add(const bz_layout* La, const bz_layout* Lb, const void* a_max, const void* a_idx,
            const void* b_max, const void* b_idx, int subtract, void* out_max,
-           void* out_idx, void* stream);
+           void* out_idx, void* out_dc, void* stream);
 /* add_scalar: shift each block's first coefficient by shift = x*sqrt(prod i)
  * then rebin (ops.py:207-215). */
 int bz_add_scalar(const bz_layout* L, const void* maxima, const void* indices, double shift,
-                  void* out_max, void* out_idx, void* stream);
+                  void* out_max, void* out_idx, void* out_dc, void* stream);
+/* DC plane of an existing array (dc[b] = indices[b][0]; stride-K gather). */
+int bz_extract_dc(const bz_layout* L, const void* indices, void* dc, void* stream);
 
 /* ---- reductions (ops.py:226-348) ---------------------------------------
  * Produce one partial record of BZ_RECORD_DOUBLES doubles (device) for the
@@ -125,6 +142,7 @@ int bz_add_scalar(const bz_layout* L, const void* maxima, const void* indices, d
  *   [4] M_aa     [5] M_bb
  *   [6] S_ab     sum over blocks Na*Nb*sum_{kept k != first} Fa_k*Fb_k
  *   [7] S_aa     [8] S_bb
+ *   [15] 1.0, stored last: the completion flag (bz_wait_record)
  * When the mask drops the first coefficient, entries 1-5 are 0 and S_* run
  * over every kept position.  Records of shards merge with Chan's formulas.
  * `pair` = 0 reads only a (b ignored; *_b and *_ab mirror a).
@@ -137,6 +155,11 @@ size_t bz_moments_workspace(const bz_layout* L);
 int bz_moments(const bz_layout* La, const bz_layout* Lb, const void* a_max, const void* a_idx,
                const void* b_max, const void* b_idx, int pair, int dc_only, double* record,
                void* workspace, size_t workspace_bytes, void* stream);
+/* The dc_only = 1 record (mean, ops.py:244-257) from the DC plane: reads
+ * B*(idx+f) contiguous bytes; bit-identical to bz_moments(dc_only = 1).
+ * Same workspace contract as bz_moments.                                    */
+int bz_moments_dc(const bz_layout* L, const void* maxima, const void* dc, double* record,
+                  void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- building blocks of the API (arrays.py, transforms.py, codec.py) --- */
 /* round_to_kind / convert_precision (kinds.py:186-206, arrays.py:147-153):

@@ -64,16 +64,20 @@ SIGNATURES = {
     "bz_last_error": (ctypes.c_char_p, []),
     "bz_launch_count": (ctypes.c_longlong, []),
     "bz_fast_path": (_I, [_L]),
+    "bz_stream_sync": (_I, [_P]),
+    "bz_wait_record": (_I, [_P, _P]),
     "bz_compress_workspace": (_SZ, [_L]),
-    "bz_compress": (_I, [_L, _P, _I, _P, _P, _P, _SZ, _P]),
+    "bz_compress": (_I, [_L, _P, _I, _P, _P, _P, _P, _SZ, _P]),
     "bz_decompress_workspace": (_SZ, [_L]),
     "bz_decompress": (_I, [_L, _P, _P, _P, _I, _P, _SZ, _P]),
     "bz_negate": (_I, [_I, _P, _P, _I64, _P]),
-    "bz_mul_scalar": (_I, [_L, _P, _P, _D, _P, _P, _P]),
-    "bz_add": (_I, [_L, _L, _P, _P, _P, _P, _I, _P, _P, _P]),
-    "bz_add_scalar": (_I, [_L, _P, _P, _D, _P, _P, _P]),
+    "bz_mul_scalar": (_I, [_L, _P, _P, _P, _D, _P, _P, _P, _P]),
+    "bz_add": (_I, [_L, _L, _P, _P, _P, _P, _I, _P, _P, _P, _P]),
+    "bz_add_scalar": (_I, [_L, _P, _P, _D, _P, _P, _P, _P]),
+    "bz_extract_dc": (_I, [_L, _P, _P, _P]),
     "bz_moments_workspace": (_SZ, [_L]),
     "bz_moments": (_I, [_L, _L, _P, _P, _P, _P, _I, _I, _P, _P, _SZ, _P]),
+    "bz_moments_dc": (_I, [_L, _P, _P, _P, _P, _SZ, _P]),
     "bz_round_to_kind": (_I, [_P, _I, _P, _I, _I64, _P, _P]),
     "bz_gradient": (_I, [_I, ctypes.POINTER(ctypes.c_int64), _I, _P, _P]),
     "bz_block": (_I, [_L, _P, _I, _P, _P]),
@@ -123,8 +127,23 @@ def load_library(require_cuda: bool = True):
     return _lib
 
 
+_raw_stream = torch._C._cuda_getCurrentRawStream
+
+
 def stream_handle(device=None) -> int:
-    return torch.cuda.current_stream(device).cuda_stream
+    """The current stream's cudaStream_t for `device` (an int; no Stream
+    object is built, which keeps per-call host overhead low)."""
+    if device is None:
+        return _raw_stream(_current_device())
+    idx = device.index if isinstance(device, torch.device) else device
+    return _raw_stream(_current_device() if idx is None else int(idx))
+
+
+def sync_stream(device=None) -> None:
+    """Wait for the current stream of `device` (only that stream), through
+    the library (cudaStreamSynchronize with the GIL released) -- a fraction
+    of the host cost of building a torch Stream object and syncing it."""
+    call("bz_stream_sync", stream_handle(device))
 
 
 def call(name: str, *args) -> int:
@@ -149,6 +168,9 @@ def _device_of(x):
     return dev
 
 
+_current_device = torch._C._cuda_getDevice
+
+
 def on_device(fn):
     """Run a public operator with its first operand's GPU current, so the
     library's launches, occupancy queries and attribute calls (which act on
@@ -158,7 +180,7 @@ def on_device(fn):
     def wrapper(a, *args, **kwargs):
         dev = _device_of(a)
         if dev is not None and dev.type == "cuda" and dev.index is not None \
-                and dev.index != torch.cuda.current_device():
+                and dev.index != _current_device():
             with torch.cuda.device(dev):
                 return fn(a, *args, **kwargs)
         return fn(a, *args, **kwargs)

@@ -236,10 +236,10 @@ class CompressedArray:
     operand's unchanged maxima or indices (negate, mul_scalar).
     """
 
-    __slots__ = ("original_shape", "settings", "maxima", "indices", "_lay")
+    __slots__ = ("original_shape", "settings", "maxima", "indices", "_lay", "_dc")
 
     def __init__(self, original_shape, settings: CodecSettings, maxima, indices, *,
-                 _trusted: bool = False):
+                 _trusted: bool = False, dc=None):
         shape = validate_shape(original_shape)
         grid = settings.grid_for(shape)
         if _trusted:
@@ -260,6 +260,9 @@ class CompressedArray:
         for k, v in (("original_shape", shape), ("settings", settings), ("maxima", m),
                      ("indices", idx)):
             object.__setattr__(self, k, v)
+        # DC plane: the first coefficient of every block, contiguous (written by
+        # the producing kernel; a cache of indices[..., 0], not part of equality)
+        object.__setattr__(self, "_dc", dc if _trusted else None)
 
     def __setattr__(self, name, value):
         raise AttributeError("CompressedArray is immutable")
@@ -275,6 +278,12 @@ class CompressedArray:
     @property
     def device(self) -> torch.device:
         return self.indices.device
+
+    @property
+    def dc_plane(self) -> torch.Tensor | None:
+        """indices[..., 0] as a contiguous grid-shaped tensor when the producing
+        kernel wrote it (compress / add / scalar ops), else None."""
+        return self._dc
 
     def maxima_f64(self) -> torch.Tensor:
         return widen(self.maxima)
@@ -335,12 +344,22 @@ def compress(a: DenseArray, settings: CodecSettings) -> CompressedArray:
     maxima = torch.empty(grid, dtype=settings.float_kind.torch_dtype, device=dev)
     indices = torch.empty(grid + (settings.mask.kept_count,), dtype=settings.index_kind.torch_dtype,
                           device=dev)
+    dc = new_dc_plane(settings, grid, dev)
     L = layout(settings, a.shape, dev)
     ws = workspace(_native.query("bz_compress_workspace", ctypes.byref(L)), dev)
     _native.call("bz_compress", ctypes.byref(L), a.values.data_ptr(), a.kind.code,
-                 maxima.data_ptr(), indices.data_ptr(), ws.data_ptr(), ws.numel(),
-                 _native.stream_handle(dev))
-    return CompressedArray(a.shape, settings, maxima, indices, _trusted=True)
+                 maxima.data_ptr(), indices.data_ptr(), _native.ptr(dc), ws.data_ptr(),
+                 ws.numel(), _native.stream_handle(dev))
+    out = CompressedArray(a.shape, settings, maxima, indices, _trusted=True, dc=dc)
+    object.__setattr__(out, "_lay", L)
+    return out
+
+
+def new_dc_plane(settings: CodecSettings, grid, device) -> torch.Tensor | None:
+    """Storage for a result's DC plane (None when the mask drops position 0)."""
+    if not settings.mask.keeps_first or settings.mask.kept_count == 0:
+        return None
+    return torch.empty(grid, dtype=settings.index_kind.torch_dtype, device=device)
 
 
 @_native.on_device

@@ -111,12 +111,10 @@ __device__ __forceinline__ void red_finish(double red_acc, double* __restrict__ 
     double s = 0.0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += wsum[i];
     red_ws[2 + blockIdx.x] = s;
-    __threadfence();
-    last = atomicAdd(reinterpret_cast<unsigned int*>(red_ws), 1u) == gridDim.x - 1;
+    last = ticket_arrive(reinterpret_cast<unsigned int*>(red_ws)) == gridDim.x - 1;
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
-    __threadfence();
     double s = 0.0;
     for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(red_ws + 2 + i);
     red_ws[1] = s;
@@ -638,11 +636,12 @@ k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
 template <typename IT>
 static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                         const void* b_max, const void* b_idx, int subtract, double shift,
-                        int mode, void* out_max, void* out_idx, cudaStream_t s) {
+                        int mode, void* out_max, void* out_idx, cudaStream_t s, void* out_dc) {
   // int8 indices with float32 maxima, whole 16-byte chunks: bz_add8.cu
   if (sizeof(IT) == 1 && add8_supported(ga, gb, mode, a_idx, b_idx, out_idx) &&
       !getenv("BZC_B200_NO_ADD8"))
-    return launch_add8(ga, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s);
+    return launch_add8(ga, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s,
+                       out_dc);
   constexpr int V = 16 / sizeof(IT);
   const int kept = ga.kept;
   const int vecs = (kept + V - 1) / V;  // chunks per block
@@ -689,9 +688,7 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
 #define BZ_TT(F, M, G, C)                                                                           \
   {                                                                                                 \
     auto kern = k_add_tiled<IT, F, M, G, C>;                                                        \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    int occ = 1;                                                                                    \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);                           \
+    const int occ = occupancy((const void*)kern, 256, smem);                                        \
     const int g2 = (int)std::min<int64_t>(ntiles, (int64_t)kSMs * std::max(occ, 1));                \
     kern<<<g2, 256, smem, s>>>(ga.nblocks, kept, tbt, a_max, (const IT*)a_idx, b_max,               \
                                (const IT*)b_idx, subtract, shift, out_max, (IT*)out_idx, nullptr);  \
@@ -719,9 +716,7 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
 #define BZ_ST(F, M)                                                                                 \
   {                                                                                                 \
     auto kern = k_add_staged<IT, F, M>;                                                             \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    int occ = 1;                                                                                    \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);                           \
+    const int occ = occupancy((const void*)kern, 256, smem);                                        \
     const int g2 = (int)std::min<int64_t>(ntiles, (int64_t)kSMs * std::max(occ, 1));                \
     kern<<<g2, 256, smem, s>>>(ga.nblocks, kept, tb, a_max, (const IT*)a_idx, b_max,                \
                                (const IT*)b_idx, subtract, shift, out_max, (IT*)out_idx);           \
@@ -798,9 +793,7 @@ static int launch_subtract_l2_t(const Geo& ga, const Geo& gb, const void* a_max,
 #define BZ_TT(F, G, C)                                                                              \
   {                                                                                                 \
     auto kern = k_add_tiled<IT, F, 0, G, C, true>;                                                  \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    int occ = 1;                                                                                    \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);                           \
+    const int occ = occupancy((const void*)kern, 256, smem);                                        \
     const int g2 = (int)std::min<int64_t>(ntiles, (int64_t)kSMs * std::min(std::max(occ, 1), 3));   \
     kern<<<g2, 256, smem, s>>>(ga.nblocks, kept, tbt, a_max, (const IT*)a_idx, b_max,               \
                                (const IT*)b_idx, 1, 0.0, nullptr, nullptr, ws);                     \
@@ -865,14 +858,23 @@ int launch_subtract_l2(const Geo& ga, const Geo& gb, const void* a_max, const vo
 
 int launch_add(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                const void* b_max, const void* b_idx, int subtract, double shift, int mode,
-               void* out_max, void* out_idx, cudaStream_t s) {
+               void* out_max, void* out_idx, cudaStream_t s, void* out_dc) {
   if (ga.nblocks == 0) return BZ_OK;
+  if (!ga.keeps_first) out_dc = nullptr;
+  // the int8 / float32 kernel writes the DC plane itself; the others are
+  // followed by a gather of the first coefficients
+  const bool own = ga.index_kind == BZ_I8 && add8_supported(ga, gb, mode, a_idx, b_idx, out_idx) &&
+                   !getenv("BZC_B200_NO_ADD8");
+  void* dc_in = own ? out_dc : nullptr;
+  int rc;
   switch (ga.index_kind) {
-    case BZ_I8: return launch_add_t<int8_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s);
-    case BZ_I16: return launch_add_t<int16_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s);
-    case BZ_I32: return launch_add_t<int32_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s);
-    default: return launch_add_t<int64_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s);
+    case BZ_I8: rc = launch_add_t<int8_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, dc_in); break;
+    case BZ_I16: rc = launch_add_t<int16_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, dc_in); break;
+    case BZ_I32: rc = launch_add_t<int32_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, dc_in); break;
+    default: rc = launch_add_t<int64_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, dc_in); break;
   }
+  if (rc || !out_dc || own) return rc;
+  return launch_extract_dc(ga, out_idx, out_dc, s);
 }
 
 }  // namespace bz

@@ -37,7 +37,8 @@ __device__ __noinline__ void add8_block_exact(int64_t b, int kept, int sub, unsi
                                               const float* __restrict__ b_max,
                                               const int8_t* __restrict__ b_idx, int subtract,
                                               double shift, float* __restrict__ out_max,
-                                              int8_t* __restrict__ out_idx) {
+                                              int8_t* __restrict__ out_idx,
+                                              int8_t* __restrict__ out_dc) {
   const double r = 127.0;
   const int64_t base = b * (int64_t)kept;
   const double na = (double)a_max[b];
@@ -60,6 +61,7 @@ __device__ __noinline__ void add8_block_exact(int64_t b, int kept, int sub, unsi
   const double n = round_to_kind<BZ_F32>(m);
   if (sub == 0) out_max[b] = (float)n;
   for (int k = sub; k < kept; k += GS) out_idx[base + k] = (int8_t)bin_exact(coeff(k), n, r, r);
+  if (out_dc && sub == 0) out_dc[b] = (int8_t)bin_exact(coeff(0), n, r, r);
 }
 
 }  // namespace
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(256, NCH == 1 ? 3 : 2)
 k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
        const int8_t* __restrict__ a_idx, const float* __restrict__ b_max,
        const int8_t* __restrict__ b_idx, int subtract, double shift,
-       float* __restrict__ out_max, int8_t* __restrict__ out_idx) {
+       float* __restrict__ out_max, int8_t* __restrict__ out_idx, int8_t* __restrict__ out_dc) {
   constexpr double r = 127.0, rinv = 1.0 / 127.0;
   constexpr int L = NCH * 16;
   const int lane = threadIdx.x & 31;
@@ -180,7 +182,10 @@ k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
     const bool bad = !safe || !bc.fast || !(m < 1.7976931348623157e308);
     const bool any_bad = (__ballot_sync(gmask, near || bad) & gmask) != 0u;
     if (!any_bad) {
-      if (sub == 0) out_max[b] = (float)n;
+      if (sub == 0) {
+        out_max[b] = (float)n;
+        if (out_dc) out_dc[b] = (int8_t)ov[0].x;  // DC plane: flat position 0
+      }
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
         const int k0 = (ch * GS + sub) * 16;
@@ -188,7 +193,7 @@ k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
       }
     } else {  // group-uniform: the exact path for this block
       add8_block_exact<GS, MODE>(b, kept, sub, gmask, a_max, a_idx, b_max, b_idx, subtract, shift,
-                                 out_max, out_idx);
+                                 out_max, out_idx, out_dc);
     }
   }
 }
@@ -204,7 +209,7 @@ bool add8_supported(const Geo& ga, const Geo& gb, int mode, const void* a_idx, c
 
 int launch_add8(const Geo& ga, const void* a_max, const void* a_idx, const void* b_max,
                 const void* b_idx, int subtract, double shift, int mode, void* out_max,
-                void* out_idx, cudaStream_t s) {
+                void* out_idx, cudaStream_t s, void* out_dc) {
   const int vecs = ga.kept / 16;
   int GS = 1;
   while (GS < 32 && GS < vecs) GS <<= 1;
@@ -214,7 +219,7 @@ int launch_add8(const Geo& ga, const void* a_max, const void* a_idx, const void*
   k_add8<G, N, M><<<grid, 256, 0, s>>>(ga.nblocks, ga.kept, (const float*)a_max,              \
                                        (const int8_t*)a_idx, (const float*)b_max,             \
                                        (const int8_t*)b_idx, subtract, shift, (float*)out_max, \
-                                       (int8_t*)out_idx)
+                                       (int8_t*)out_idx, (int8_t*)out_dc)
 #define BZ_A8M(G, N) \
   do { if (mode == 0) BZ_A8(G, N, 0); else BZ_A8(G, N, 1); } while (0)
 #define BZ_A8G(G)             \

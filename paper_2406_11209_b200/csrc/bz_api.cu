@@ -1,5 +1,8 @@
 // bz_api.cu -- extern "C" entry points (include/bzc_b200.h).
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -28,6 +31,33 @@ int check_launch(const char* what) {
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return BZ_OK;
+}
+
+int occupancy(const void* kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, size_t>, int> occ_cache;
+  static std::map<std::pair<int, const void*>, size_t> smem_attr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, kern, threads, smem);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = occ_cache.find(key);
+  if (it != occ_cache.end()) return it->second;
+  if (smem > 48 * 1024) {
+    size_t& cur = smem_attr[{dev, kern}];
+    if (smem > cur) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cur = smem;
+    }
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    occ = 1;
+  }
+  occ = occ < 1 ? 1 : occ;
+  occ_cache[key] = occ;
+  return occ;
 }
 
 static int validate(const bz_layout* L) {
@@ -80,6 +110,34 @@ int bz_version(void) { return 10000; }
 long long bz_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 const char* bz_last_error(void) { return g_err; }
 
+int bz_stream_sync(void* stream) {
+  cudaError_t e = cudaStreamSynchronize(S(stream));
+  if (e != cudaSuccess) {
+    set_error("stream sync: %s", cudaGetErrorString(e));
+    return BZ_E_CUDA;
+  }
+  return BZ_OK;
+}
+
+int bz_wait_record(const double* record, void* stream) {
+  const volatile double* flag = record + BZ_RECORD_DOUBLES - 1;
+  for (unsigned spin = 1;; ++spin) {
+    if (*flag == 1.0) return BZ_OK;
+    if ((spin & 1023u) == 0) {  // every ~1k polls: has the stream finished or failed?
+      cudaError_t e = cudaStreamQuery(S(stream));
+      if (e == cudaSuccess) {
+        if (*flag == 1.0) return BZ_OK;
+        set_error("wait_record: stream idle but the record is not complete");
+        return BZ_E_INVALID;
+      }
+      if (e != cudaErrorNotReady) {
+        set_error("wait_record: %s", cudaGetErrorString(e));
+        return BZ_E_CUDA;
+      }
+    }
+  }
+}
+
 int bz_fast_path(const bz_layout* L) {
   if (validate(L)) return 0;
   Geo g = make_geo(L);
@@ -98,13 +156,27 @@ size_t bz_compress_workspace(const bz_layout* L) {
                   std::max(dct8_compress_workspace(g), dct4_compress_workspace(g))) + 256;
 }
 
+static int compress_body(const bz_layout* L, const Geo& g, const void* x, int x_kind,
+                         void* maxima, void* indices, void* dc, bool& dc_done, void* ws,
+                         size_t ws_bytes, cudaStream_t s);
+
 int bz_compress(const bz_layout* L, const void* x, int x_kind, void* maxima, void* indices,
-                void* ws, size_t ws_bytes, void* stream) {
+                void* dc, void* ws, size_t ws_bytes, void* stream) {
   if (int rc = validate(L)) return rc;
   if (int rc = need_matrices(L)) return rc;
   Geo g = make_geo(L);
   if (g.nblocks == 0) return BZ_OK;
-  cudaStream_t s = S(stream);
+  if (!g.keeps_first || g.kept == 0) dc = nullptr;
+  bool dc_done = false;
+  if (int rc = compress_body(L, g, x, x_kind, maxima, indices, dc, dc_done, ws, ws_bytes, S(stream)))
+    return rc;
+  return (dc && !dc_done) ? launch_extract_dc(g, indices, dc, S(stream)) : BZ_OK;
+}
+
+// dc_done: the kernel wrote the DC plane itself (factored and generic paths)
+static int compress_body(const bz_layout* L, const Geo& g, const void* x, int x_kind,
+                         void* maxima, void* indices, void* dc, bool& dc_done, void* ws,
+                         size_t ws_bytes, cudaStream_t s) {
   // input of another kind: convert_precision first (arrays.py:147-153)
   if (x_kind != L->float_kind && !force_generic() && fast_supported(g, L->float_kind)) {
     size_t need = (size_t)dense_count(L) * float_kind_bytes(L->float_kind);
@@ -113,15 +185,20 @@ int bz_compress(const bz_layout* L, const void* x, int x_kind, void* maxima, voi
     return launch_fast_compress(g, ws, maxima, indices, s);
   }
   if (!force_generic() && dct8_compress_supported(g, x_kind) && ws &&
-      ws_bytes >= dct8_compress_workspace(g))
-    return launch_dct8_compress(g, x, maxima, indices, ws, ws_bytes, s);
+      ws_bytes >= dct8_compress_workspace(g)) {
+    dc_done = true;
+    return launch_dct8_compress(g, x, maxima, indices, ws, ws_bytes, s, dc);
+  }
   if (!force_generic() && dct4_compress_supported(g, x_kind) && ws &&
-      ws_bytes >= dct4_compress_workspace(g))
-    return launch_dct4_compress(g, x, maxima, indices, ws, ws_bytes, s);
+      ws_bytes >= dct4_compress_workspace(g)) {
+    dc_done = true;
+    return launch_dct4_compress(g, x, maxima, indices, ws, ws_bytes, s, dc);
+  }
   if (!force_generic() && fast_supported(g, x_kind))
     return launch_fast_compress(g, x, maxima, indices, s);
+  dc_done = true;
   return launch_exact_compress(g, x, x_kind, maxima, indices, nullptr, nullptr, g.nblocks, ws,
-                               ws_bytes, s);
+                               ws_bytes, s, dc);
 }
 
 size_t bz_decompress_workspace(const bz_layout* L) {
@@ -152,20 +229,32 @@ int bz_negate(int index_kind, const void* in, void* out, int64_t count, void* st
   return launch_negate(index_kind, in, out, count, S(stream));
 }
 
-int bz_mul_scalar(const bz_layout* L, const void* maxima, const void* indices, double x,
-                  void* maxima_out, void* indices_out, void* stream) {
+int bz_mul_scalar(const bz_layout* L, const void* maxima, const void* indices, const void* dc,
+                  double x, void* maxima_out, void* indices_out, void* dc_out, void* stream) {
   if (int rc = validate(L)) return rc;
-  return launch_mul_scalar(make_geo(L), maxima, indices, x, maxima_out, indices_out, S(stream));
+  Geo g = make_geo(L);
+  if (int rc = launch_mul_scalar(g, maxima, indices, x, maxima_out, indices_out, S(stream))) return rc;
+  if (dc && dc_out && !(x > 0)) {  // the plane follows the indices' sign change
+    Geo gp = g;
+    gp.kept = 1;
+    return launch_mul_scalar_indices(gp, dc, x, dc_out, S(stream));
+  }
+  return BZ_OK;
 }
 
 int bz_add(const bz_layout* La, const bz_layout* Lb, const void* a_max, const void* a_idx,
            const void* b_max, const void* b_idx, int subtract, void* out_max, void* out_idx,
-           void* stream) {
+           void* out_dc, void* stream) {
   if (int rc = validate(La)) return rc;
   if (int rc = validate(Lb)) return rc;
   if (int rc = check_pair(La, Lb, "add", true)) return rc;
   return launch_add(make_geo(La), make_geo(Lb), a_max, a_idx, b_max, b_idx, subtract, 0.0, 0,
-                    out_max, out_idx, S(stream));
+                    out_max, out_idx, S(stream), out_dc);
+}
+
+int bz_extract_dc(const bz_layout* L, const void* indices, void* dc, void* stream) {
+  if (int rc = validate(L)) return rc;
+  return launch_extract_dc(make_geo(L), indices, dc, S(stream));
 }
 
 size_t bz_subtract_l2_workspace(void) { return subtract_l2_workspace(); }
@@ -181,12 +270,12 @@ int bz_subtract_l2(const bz_layout* La, const bz_layout* Lb, const void* a_max, 
 }
 
 int bz_add_scalar(const bz_layout* L, const void* maxima, const void* indices, double shift,
-                  void* out_max, void* out_idx, void* stream) {
+                  void* out_max, void* out_idx, void* out_dc, void* stream) {
   if (int rc = validate(L)) return rc;
   if (!L->keeps_first) { set_error("add_scalar: mask drops the first coefficient"); return BZ_E_INVALID; }
   Geo g = make_geo(L);
   return launch_add(g, g, maxima, indices, nullptr, nullptr, 0, shift, 1, out_max, out_idx,
-                    S(stream));
+                    S(stream), out_dc);
 }
 
 size_t bz_moments_workspace(const bz_layout* L) {
@@ -205,6 +294,12 @@ int bz_moments(const bz_layout* La, const bz_layout* Lb, const void* a_max, cons
   }
   return launch_moments(make_geo(La), make_geo(lb), a_max, a_idx, pair ? b_max : a_max,
                         pair ? b_idx : a_idx, pair, dc_only, record, ws, ws_bytes, S(stream));
+}
+
+int bz_moments_dc(const bz_layout* L, const void* maxima, const void* dc, double* record,
+                  void* ws, size_t ws_bytes, void* stream) {
+  if (int rc = validate(L)) return rc;
+  return launch_moments_plane(make_geo(L), maxima, dc, record, ws, ws_bytes, S(stream));
 }
 
 int bz_round_to_kind(const void* in, int in_kind, void* out, int out_kind, int64_t n,

@@ -17,6 +17,31 @@ constexpr int kSMs = 148;  // B200
 // ------------------------------------------------------------------ errors --
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
+// Resident CTAs per SM for (kernel, threads, dynamic smem) on the current
+// device, cached (the occupancy query and the smem attribute cost
+// microseconds of host time per launch); raises the kernel's dynamic-smem
+// limit to `smem` once per device when it exceeds 48 KB.
+int occupancy(const void* kern, int threads, size_t smem);
+
+// Arrival ticket of a last-CTA reduction: atomic add with acquire-release
+// semantics at GPU scope.  The release orders this thread's earlier stores
+// (its CTA's partial) before the increment; the acquire, followed by a
+// CTA barrier, orders the last CTA's later reads of every partial after it.
+// (__threadfence() is a sequentially consistent fence -- MEMBAR.SC.GPU --
+// measured at several microseconds per CTA of a short reduction.)
+__device__ __forceinline__ unsigned ticket_arrive(unsigned* counter) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(counter) : "memory");
+  return old;
+}
+
+// The last entry of a reduction record is its completion flag, stored after
+// every other entry with a system-scope release: a host polling a record in
+// pinned (mapped) memory reads the values once it sees 1.0 (bz_wait_record).
+__device__ __forceinline__ void record_complete(double* record) {
+  __threadfence_system();
+  *reinterpret_cast<volatile double*>(record + BZ_RECORD_DOUBLES - 1) = 1.0;
+}
 
 // ------------------------------------------------------------- kind traits --
 template <int K> struct FloatKind;

@@ -113,7 +113,8 @@ __device__ __forceinline__ void dct4_compress_pair(double (&v)[16], const int16_
                                                    void* __restrict__ maxima,
                                                    int8_t* __restrict__ indices,
                                                    int32_t* __restrict__ list,
-                                                   int32_t* __restrict__ count) {
+                                                   int32_t* __restrict__ count,
+                                                   int8_t* __restrict__ dc) {
   using namespace d4;
   const int lane = cx.lane, bs = cx.bs, o = cx.o, K = cx.K;
   const Dct4K KC = cx.KC;
@@ -195,6 +196,8 @@ __device__ __forceinline__ void dct4_compress_pair(double (&v)[16], const int16_
     } else {
       for (int e2 = lane; e2 < nbytes; e2 += 32) dst[e2] = stg[e2];
     }
+    // DC plane (passed only when the mask keeps position 0, rank 0)
+    if (dc && lane < nv) dc[b0 + lane] = stg[lane * K];
   }
 }
 
@@ -203,7 +206,7 @@ template <int FK>
 __global__ void __launch_bounds__(256, 3)
 k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restrict__ maxima,
                 int8_t* __restrict__ indices, int32_t* __restrict__ list,
-                int32_t* __restrict__ count) {
+                int32_t* __restrict__ count, int8_t* __restrict__ dc) {
   using namespace d4;
   const FastGeo& f = p.f;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -293,7 +296,7 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
                                  ? (double)src[a0 * s0 + a3] : 0.0;
       }
     }
-    dct4_compress_pair<FK>(v, rk, cx, wt * BPW, b, valid, maxima, indices, list, count);
+    dct4_compress_pair<FK>(v, rk, cx, wt * BPW, b, valid, maxima, indices, list, count, dc);
     __syncwarp();  // staging and exchange area reused by the next tile
   }
 }
@@ -324,7 +327,8 @@ template <int FK>
 __global__ void __launch_bounds__(d4t::NT, 2)
 k_dct4_compress_tma(const __grid_constant__ CUtensorMap xmap, const FastParams p,
                     void* __restrict__ maxima, int8_t* __restrict__ indices,
-                    int32_t* __restrict__ list, int32_t* __restrict__ count) {
+                    int32_t* __restrict__ list, int32_t* __restrict__ count,
+                    int8_t* __restrict__ dc) {
   using namespace d4;
   using namespace d4t;
   const FastGeo& f = p.f;
@@ -412,7 +416,7 @@ k_dct4_compress_tma(const __grid_constant__ CUtensorMap xmap, const FastParams p
       v[a0 * 4 + 3] = (double)r[a0].w;
     }
     const int64_t b0 = tile * TB + 2 * w;
-    dct4_compress_pair<FK>(v, rk, cx, b0, b0 + bs, true, maxima, indices, list, count);
+    dct4_compress_pair<FK>(v, rk, cx, b0, b0 + bs, true, maxima, indices, list, count, dc);
     __syncwarp();  // staging and exchange area reused by the next tile
   }
 }
@@ -566,8 +570,10 @@ bool dct4_compress_supported(const Geo& g, int x_kind) {
 size_t dct4_compress_workspace(const Geo& g) { return 256 + (size_t)g.nblocks * sizeof(int32_t); }
 
 int launch_dct4_compress(const Geo& g, const void* x, void* maxima, void* indices, void* ws,
-                         size_t ws_bytes, cudaStream_t s) {
+                         size_t ws_bytes, cudaStream_t s, void* dc) {
   using namespace d4;
+  if (!g.keeps_first) dc = nullptr;
+  int8_t* dc8 = reinterpret_cast<int8_t*>(dc);
   if (ws_bytes < dct4_compress_workspace(g)) { set_error("dct4 compress: workspace too small"); return BZ_E_WORKSPACE; }
   FastParams p;
   if (!make_fast_params(g, BPW * WPC, x, 4, p)) { set_error("dct4 compress: host matrices missing"); return BZ_E_INVALID; }
@@ -580,29 +586,26 @@ int launch_dct4_compress(const Geo& g, const void* x, void* maxima, void* indice
   if (!getenv("BZC_B200_NO_TMA") && g.grid[3] % d4t::TB == 0 && g.shape[3] == 4 * g.grid[3] &&
       tma::encode_f32(&xmap, x, 4, g.shape, box)) {
     auto kern = k_dct4_compress_tma<BZ_F32>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d4t::kSmem);
-    int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, d4t::NT, d4t::kSmem);
+    const int occ = occupancy((const void*)kern, d4t::NT, d4t::kSmem);
     const int64_t ntiles = g.nblocks / d4t::TB;
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)kSMs * std::max(occ, 1));
     kern<<<(int)grid, d4t::NT, d4t::kSmem, s>>>(xmap, p, maxima,
-                                                 reinterpret_cast<int8_t*>(indices), list, count);
+                                                 reinterpret_cast<int8_t*>(indices), list, count,
+                                                 dc8);
     if (int rc = check_launch("dct4_compress_tma")) return rc;
     return launch_exact_compress(g, x, BZ_F32, maxima, indices, list, count,
-                                 std::min<int64_t>(g.nblocks, 4 * kSMs), nullptr, 0, s);
+                                 std::min<int64_t>(g.nblocks, 4 * kSMs), nullptr, 0, s, dc);
   }
   const size_t smem = (size_t)WPC * BPW * XS * 8 + (size_t)WPC * BPW * SS + (size_t)4 * NT * 16;
   auto kern = k_dct4_compress<BZ_F32>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+  const int occ = occupancy((const void*)kern, NT, smem);
   const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));
   kern<<<(int)grid, NT, smem, s>>>(p, reinterpret_cast<const float*>(x), maxima,
-                                   reinterpret_cast<int8_t*>(indices), list, count);
+                                   reinterpret_cast<int8_t*>(indices), list, count, dc8);
   if (int rc = check_launch("dct4_compress")) return rc;
   // exact fix-up of flagged blocks: the generic kernel (reference FMA chain)
   return launch_exact_compress(g, x, BZ_F32, maxima, indices, list, count,
-                               std::min<int64_t>(g.nblocks, 4 * kSMs), nullptr, 0, s);
+                               std::min<int64_t>(g.nblocks, 4 * kSMs), nullptr, 0, s, dc);
 }
 
 int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
@@ -617,9 +620,7 @@ int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices
 #define BZ_D(IT, FKV, TO)                                                                     \
   {                                                                                           \
     auto kern = k_dct4_decompress<IT, FKV, TO>;                                               \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    int occ = 1;                                                                              \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);                      \
+    const int occ = occupancy((const void*)kern, NT, smem);                                         \
     const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));    \
     kern<<<(int)grid, NT, smem, s>>>(p, maxima, reinterpret_cast<const IT*>(indices),         \
                                      reinterpret_cast<TO*>(out));                             \

@@ -139,7 +139,7 @@ template <typename TIn, int FK>
 __global__ void __launch_bounds__(256, 2)
 k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict__ maxima,
                 int8_t* __restrict__ indices, int32_t* __restrict__ list,
-                int32_t* __restrict__ count) {
+                int32_t* __restrict__ count, int8_t* __restrict__ dc) {
   using namespace d8;
   const FastGeo& f = p.f;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -312,7 +312,10 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
     bad = bad || min(min(z4[0], z4[1]), min(z4[2], z4[3])) <= 2u;
     const unsigned badmask = __ballot_sync(0xffffffffu, bad && valid);
     if (valid) {
-      if (o == 0) store_kind<FK>(maxima, b, n);
+      if (o == 0) {
+        store_kind<FK>(maxima, b, n);
+        if (dc) dc[b] = (int8_t)(y[0] >> 24);  // DC plane: canonical position 0
+      }
       int8_t* dst = indices + b * (int64_t)BS + hi * 64 + h * 32;
       uint4 wv[2];
 #pragma unroll
@@ -340,7 +343,7 @@ template <typename TIn, int FK>
 __global__ void __launch_bounds__(512)
 k_dct8_fixup(const FastParams p, const TIn* __restrict__ x, void* __restrict__ maxima,
              int8_t* __restrict__ indices, const int32_t* __restrict__ list,
-             const int32_t* __restrict__ count) {
+             const int32_t* __restrict__ count, int8_t* __restrict__ dc) {
   const FastGeo& f = p.f;
   __shared__ double A[512], B[512];
   __shared__ double wm[16];
@@ -378,7 +381,9 @@ k_dct8_fixup(const FastParams p, const TIn* __restrict__ x, void* __restrict__ m
     for (int j = 1; j < 16; ++j) m = nanmax_abs(m, wm[j]);
     const double nst = round_to_kind<FK>(m);
     if (t == 0) store_kind<FK>(maxima, b, nst);
-    indices[b * 512 + t] = (int8_t)bin_exact(acc, nst, 127.0, 127.0);
+    const int8_t q = (int8_t)bin_exact(acc, nst, 127.0, 127.0);
+    indices[b * 512 + t] = q;
+    if (dc && t == 0) dc[b] = q;
     __syncthreads();  // A / wm reused
   }
 }
@@ -532,7 +537,7 @@ bool dct8_compress_supported(const Geo& g, int x_kind) {
 size_t dct8_compress_workspace(const Geo& g) { return 256 + (size_t)g.nblocks * sizeof(int32_t); }
 
 int launch_dct8_compress(const Geo& g, const void* x, void* maxima, void* indices, void* ws,
-                         size_t ws_bytes, cudaStream_t s) {
+                         size_t ws_bytes, cudaStream_t s, void* dc) {
   using namespace d8;
   if (ws_bytes < dct8_compress_workspace(g)) { set_error("dct8 compress: workspace too small"); return BZ_E_WORKSPACE; }
   FastParams p;
@@ -543,16 +548,16 @@ int launch_dct8_compress(const Geo& g, const void* x, void* maxima, void* indice
   if (cudaMemsetAsync(count, 0, sizeof(int32_t), s) != cudaSuccess) return check_launch("dct8 memset");
   const size_t smem = (size_t)WPC * BPW * BS * 8 + stage_bytes;
   auto kern = k_dct8_compress<float, BZ_F32>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+  const int occ = occupancy((const void*)kern, NT, smem);
   const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));
   kern<<<(int)grid, NT, smem, s>>>(p, reinterpret_cast<const float*>(x), maxima,
-                                   reinterpret_cast<int8_t*>(indices), list, count);
+                                   reinterpret_cast<int8_t*>(indices), list, count,
+                                   reinterpret_cast<int8_t*>(dc));
   if (int rc = check_launch("dct8_compress")) return rc;
   // exact fix-up of flagged blocks (the reference FMA chain)
   k_dct8_fixup<float, BZ_F32><<<2 * kSMs, 512, 0, s>>>(p, reinterpret_cast<const float*>(x), maxima,
-                                                        reinterpret_cast<int8_t*>(indices), list, count);
+                                                        reinterpret_cast<int8_t*>(indices), list, count,
+                                                        reinterpret_cast<int8_t*>(dc));
   return check_launch("dct8_fixup");
 }
 
@@ -568,9 +573,7 @@ int launch_dct8_decompress(const Geo& g, const void* maxima, const void* indices
 #define BZ_D(IT, FKV, TO)                                                                     \
   {                                                                                           \
     auto kern = k_dct8_decompress<IT, FKV, TO>;                                               \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    int occ = 1;                                                                              \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);                      \
+    const int occ = occupancy((const void*)kern, NT, smem);                                         \
     const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));    \
     kern<<<(int)grid, NT, smem, s>>>(p, maxima, reinterpret_cast<const IT*>(indices),         \
                                      reinterpret_cast<TO*>(out));                             \

@@ -288,10 +288,7 @@ static int launch_one(const Geo& g, const void* x, void* maxima, void* indices, 
                                      ((size_t)TL::BS * 2 + 15) / 16 * 16) +
                 0 * (size_t)TL::NT * ROWS * RU * 16;  // PREFETCH stage (disabled)
   auto kern = k_fast_compress<D, E, TIn, FK, IT>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TL::NT, smem);
-  if (occ < 1) occ = 1;
+  const int occ = occupancy((const void*)kern, TL::NT, smem);
   int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * occ);
   if (grid < 1) return BZ_OK;
   kern<<<(int)grid, TL::NT, smem, s>>>(p, reinterpret_cast<const TIn*>(x), maxima,

@@ -284,10 +284,7 @@ static int launch_one(const Geo& g, const void* maxima, const void* indices, voi
                      ? 2 * (((size_t)TL::BPC * g.kept * sizeof(IT) + 16 + 15) / 16 * 16) : 0) +
                 (p.f.full_mask ? 0 : (size_t)TL::BS * 2 + 16);
   auto kern = k_fast_decompress<D, E, IT, FK, TOut>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TL::NT, smem);
-  if (occ < 1) occ = 1;
+  const int occ = occupancy((const void*)kern, TL::NT, smem);
   int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * occ);
   if (grid < 1) return BZ_OK;
   kern<<<(int)grid, TL::NT, smem, s>>>(p, maxima, reinterpret_cast<const IT*>(indices),

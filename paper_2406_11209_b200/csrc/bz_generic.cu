@@ -246,7 +246,8 @@ __device__ void exact_compress_block(const Geo& g, const void* x, int x_kind, in
 }
 
 __global__ void k_exact_compress(Geo g, const void* x, int x_kind, void* maxima, void* indices,
-                                 double* gscratch, const int32_t* list, const int32_t* count) {
+                                 double* gscratch, const int32_t* list, const int32_t* count,
+                                 void* dc) {
   extern __shared__ double smem[];
   const int wib = threadIdx.x >> 5;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -257,7 +258,33 @@ __global__ void k_exact_compress(Geo g, const void* x, int x_kind, void* maxima,
   for (int64_t w = warp; w < total; w += nwarps) {
     int64_t b = list ? (int64_t)list[w] : w;
     exact_compress_block(g, x, x_kind, b, A, B, maxima, indices);
+    // DC plane: lane 0 stored flat position 0 (the first coefficient)
+    if (dc && (threadIdx.x & 31) == 0)
+      store_index_rt(dc, b, load_index_rt(indices, b * g.kept, g.index_kind), g.index_kind);
   }
+}
+
+// DC plane from the indices: dc[b] = F[b][0] (strided gather; the producers
+// that know F0 in registers write the plane themselves)
+template <typename IT>
+__global__ void k_extract_dc(int64_t nblocks, int kept, const IT* __restrict__ indices,
+                             IT* __restrict__ dc) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblocks;
+       b += (int64_t)gridDim.x * blockDim.x)
+    dc[b] = __ldcs(indices + b * (int64_t)kept);
+}
+
+int launch_extract_dc(const Geo& g, const void* indices, void* dc, cudaStream_t s) {
+  if (!dc || g.nblocks == 0) return BZ_OK;
+  if (!g.keeps_first) { set_error("extract_dc: mask drops the first coefficient"); return BZ_E_INVALID; }
+  const int grid = grid_for(g.nblocks, 256, 8);
+  switch (g.index_kind) {
+    case BZ_I8: k_extract_dc<<<grid, 256, 0, s>>>(g.nblocks, g.kept, (const int8_t*)indices, (int8_t*)dc); break;
+    case BZ_I16: k_extract_dc<<<grid, 256, 0, s>>>(g.nblocks, g.kept, (const int16_t*)indices, (int16_t*)dc); break;
+    case BZ_I32: k_extract_dc<<<grid, 256, 0, s>>>(g.nblocks, g.kept, (const int32_t*)indices, (int32_t*)dc); break;
+    default: k_extract_dc<<<grid, 256, 0, s>>>(g.nblocks, g.kept, (const int64_t*)indices, (int64_t*)dc); break;
+  }
+  return check_launch("extract_dc");
 }
 
 // ------------------------------------- exact per-block decompress (warp) --
@@ -317,7 +344,8 @@ size_t exact_scratch_bytes(const Geo& g, int blocks_in_grid, bool& use_smem) {
 
 int launch_exact_compress(const Geo& g, const void* x, int x_kind, void* maxima, void* indices,
                           const int32_t* list, const int32_t* count, int64_t max_blocks,
-                          void* ws, size_t ws_bytes, cudaStream_t s) {
+                          void* ws, size_t ws_bytes, cudaStream_t s, void* dc) {
+  if (dc && !g.keeps_first) dc = nullptr;
   bool use_smem;
   int grid = grid_for(max_blocks, kGenericWarps, 16);
   size_t need = exact_scratch_bytes(g, grid, use_smem);
@@ -329,11 +357,10 @@ int launch_exact_compress(const Geo& g, const void* x, int x_kind, void* maxima,
     need = per_cta * grid;
   }
   size_t smem = use_smem ? 2 * (size_t)g.bsize * sizeof(double) * kGenericWarps : 0;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_exact_compress, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024) occupancy((const void*)k_exact_compress, 32 * kGenericWarps, smem);
   k_exact_compress<<<grid, 32 * kGenericWarps, smem, s>>>(g, x, x_kind, maxima, indices,
                                                            use_smem ? nullptr : (double*)ws, list,
-                                                           count);
+                                                           count, dc);
   (void)need;
   return check_launch("exact_compress");
 }
@@ -355,9 +382,7 @@ int launch_exact_decompress(const Geo& g, const void* maxima, const void* indice
     grid = (int)std::min<size_t>((size_t)grid, ws_bytes / per_cta);
   }
   size_t smem = use_smem ? 2 * (size_t)g.bsize * sizeof(double) * kGenericWarps : 0;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_exact_decompress, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+  if (smem > 48 * 1024) occupancy((const void*)k_exact_decompress, 32 * kGenericWarps, smem);
   k_exact_decompress<<<grid, 32 * kGenericWarps, smem, s>>>(
       g, maxima, indices, out, out_kind, use_smem ? nullptr : (double*)ws);
   return check_launch("exact_decompress");

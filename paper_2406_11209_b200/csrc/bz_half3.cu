@@ -369,9 +369,7 @@ static int launch_c(const Geo& g, const void* x, void* maxima, void* indices, cu
   size_t smem = (size_t)BPC * BSP * 8 + (size_t)NT * 8 +
                 (p.f.full_mask ? 0 : ((size_t)BPC * g.kept * sizeof(IT) + 16 + 15) / 16 * 16 + BS * 2);
   auto kern = k_half3_compress<TIn, FK, IT>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+  const int occ = occupancy((const void*)kern, NT, smem);
   const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));
   if (grid < 1) return BZ_OK;
   kern<<<(int)grid, NT, smem, s>>>(p, reinterpret_cast<const TIn*>(x), maxima,
@@ -391,9 +389,7 @@ static int launch_d(const Geo& g, const void* maxima, const void* indices, void*
   size_t smem = (size_t)BPC * BSP * 8 + ((size_t)BPC * g.kept * sizeof(IT) + 32 + 15) / 16 * 16 +
                 (p.f.full_mask ? 0 : BS * 2);
   auto kern = k_half3_decompress<IT, FK, TOut>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+  const int occ = occupancy((const void*)kern, NT, smem);
   const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));
   if (grid < 1) return BZ_OK;
   kern<<<(int)grid, NT, smem, s>>>(p, maxima, reinterpret_cast<const IT*>(indices),

@@ -25,7 +25,9 @@ int launch_specified(const Geo& g, const void* maxima, const void* flat, double*
                      cudaStream_t s);
 int launch_exact_compress(const Geo& g, const void* x, int x_kind, void* maxima, void* indices,
                           const int32_t* list, const int32_t* count, int64_t max_blocks,
-                          void* ws, size_t ws_bytes, cudaStream_t s);
+                          void* ws, size_t ws_bytes, cudaStream_t s, void* dc = nullptr);
+// DC plane (dc[b] = F[b][0], contiguous): gather from the indices
+int launch_extract_dc(const Geo& g, const void* indices, void* dc, cudaStream_t s);
 size_t exact_compress_workspace(const Geo& g, int64_t max_blocks);
 int launch_exact_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                             int out_kind, void* ws, size_t ws_bytes, cudaStream_t s);
@@ -46,7 +48,7 @@ bool dct8_supported(const Geo& g);
 bool dct8_compress_supported(const Geo& g, int x_kind);
 size_t dct8_compress_workspace(const Geo& g);
 int launch_dct8_compress(const Geo& g, const void* x, void* maxima, void* indices, void* ws,
-                         size_t ws_bytes, cudaStream_t s);
+                         size_t ws_bytes, cudaStream_t s, void* dc = nullptr);
 int launch_dct8_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s);
 
@@ -55,7 +57,7 @@ bool dct4_supported(const Geo& g);
 bool dct4_compress_supported(const Geo& g, int x_kind);
 size_t dct4_compress_workspace(const Geo& g);
 int launch_dct4_compress(const Geo& g, const void* x, void* maxima, void* indices, void* ws,
-                         size_t ws_bytes, cudaStream_t s);
+                         size_t ws_bytes, cudaStream_t s, void* dc = nullptr);
 int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices, void* out,
                            int out_kind, cudaStream_t s);
 
@@ -83,16 +85,18 @@ int launch_stream_unpack(const void* in, int64_t in_words, int64_t bit_offset, v
 
 // compressed-domain ops (bz_ops.cu)
 int launch_negate(int ik, const void* in, void* out, int64_t n, cudaStream_t s);
+int launch_mul_scalar_indices(const Geo& g, const void* indices, double x, void* indices_out,
+                              cudaStream_t s);
 int launch_mul_scalar(const Geo& g, const void* maxima, const void* indices, double x,
                       void* maxima_out, void* indices_out, cudaStream_t s);
 bool add8_supported(const Geo& ga, const Geo& gb, int mode, const void* a_idx, const void* b_idx,
                     const void* out_idx);
 int launch_add8(const Geo& ga, const void* a_max, const void* a_idx, const void* b_max,
                 const void* b_idx, int subtract, double shift, int mode, void* out_max,
-                void* out_idx, cudaStream_t s);
+                void* out_idx, cudaStream_t s, void* out_dc = nullptr);
 int launch_add(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                const void* b_max, const void* b_idx, int subtract, double shift, int mode,
-               void* out_max, void* out_idx, cudaStream_t s);
+               void* out_max, void* out_idx, cudaStream_t s, void* out_dc = nullptr);
 size_t subtract_l2_workspace();
 int launch_subtract_l2(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                        const void* b_max, const void* b_idx, double* out, void* ws,
@@ -101,5 +105,8 @@ size_t moments_workspace(const Geo& g);
 int launch_moments(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                    const void* b_max, const void* b_idx, int pair, int dc_only, double* record,
                    void* ws, size_t ws_bytes, cudaStream_t s);
+// mean record from the DC plane (contiguous first coefficients)
+int launch_moments_plane(const Geo& g, const void* maxima, const void* dc, double* record,
+                         void* ws, size_t ws_bytes, cudaStream_t s);
 
 }  // namespace bz

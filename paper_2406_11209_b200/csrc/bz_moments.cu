@@ -187,12 +187,10 @@ __device__ __forceinline__ void finish(Rec r, double* __restrict__ ws, int pair,
   __shared__ bool last;
   if (threadIdx.x == 0) {
     store_rec(recs + blockIdx.x * BZ_RECORD_DOUBLES, t);
-    __threadfence();
-    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    last = ticket_arrive(counter) == gridDim.x - 1;
   }
   __syncthreads();
   if (!last) return;
-  __threadfence();
   const int per = (gridDim.x + blockDim.x - 1) / blockDim.x;
   Rec m = rec_zero();
   for (int i = threadIdx.x * per; i < min((int)gridDim.x, (int)(threadIdx.x + 1) * per); ++i) {
@@ -204,7 +202,8 @@ __device__ __forceinline__ void finish(Rec r, double* __restrict__ ws, int pair,
   if (threadIdx.x == 0) {
     if (!pair) { f.mb = f.ma; f.Mab = f.Maa; f.Mbb = f.Maa; f.Sab = f.Saa; f.Sbb = f.Saa; }
     store_rec(record, f);
-    for (int i = 9; i < BZ_RECORD_DOUBLES; ++i) record[i] = 0.0;
+    for (int i = 9; i < BZ_RECORD_DOUBLES - 1; ++i) record[i] = 0.0;
+    record_complete(record);
     *counter = 0u;  // re-arm for the next launch on this workspace
   }
 }
@@ -572,7 +571,7 @@ k_moments_staged(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
 // ------------------------------------------------- first coefficients only --
 template <typename IT, int U, bool PAIR>
 __global__ void __launch_bounds__(256, 2)
-k_moments_dc(int64_t nblocks, int kept, int fk_a, int fk_b, const void* __restrict__ a_max,
+k_moments_dc(int64_t nblocks, int64_t kept, int fk_a, int fk_b, const void* __restrict__ a_max,
              const IT* __restrict__ a_idx, const void* __restrict__ b_max,
              const IT* __restrict__ b_idx, double* __restrict__ ws,
              double* __restrict__ record) {
@@ -585,9 +584,9 @@ k_moments_dc(int64_t nblocks, int kept, int fk_a, int fk_b, const void* __restri
     for (int u = 0; u < U; ++u) {
       const int64_t b = bb + u * nth;
       const bool ok = b < nblocks;
-      fa[u] = ok ? (double)__ldcs(a_idx + b * (int64_t)kept) : 0.0;
+      fa[u] = ok ? (double)__ldcs(a_idx + b * kept) : 0.0;
       na[u] = ok ? load_kind_rt(a_max, b, fk_a) : 0.0;
-      fb[u] = (ok && PAIR) ? (double)__ldcs(b_idx + b * (int64_t)kept) : fa[u];
+      fb[u] = (ok && PAIR) ? (double)__ldcs(b_idx + b * kept) : fa[u];
       nb[u] = (ok && PAIR) ? load_kind_rt(b_max, b, fk_b) : na[u];
     }
 #pragma unroll
@@ -595,6 +594,118 @@ k_moments_dc(int64_t nblocks, int kept, int fk_a, int fk_b, const void* __restri
       if (bb + u * nth < nblocks) st.add_block<PAIR>(0, 0, 0, fa[u], fb[u], na[u], nb[u], true);
   }
   finish(st.record(true), ws, PAIR, record);
+}
+
+// DC plane (mean, ops.py:244-257): each thread owns runs of 16 consecutive
+// blocks -- their first coefficients arrive as 16-byte vectors (one per
+// 16 / sizeof(IT) blocks) and the float32 / float64 maxima as 16-byte
+// vectors too, U runs in flight per thread and one wave of CTAs, so the
+// B*(idx+f) bytes stream at full width.  Every DC value x = F0*N is shifted
+// by one global pivot p (block 0's value, which every thread loads), so a
+// partial is just (count, sum(x-p), sum((x-p)^2)) and partials merge by
+// plain addition -- a three-double tree instead of a Chan merge of the full
+// record.  The last CTA adds the CTA partials in index order
+// (deterministic) and writes the record's entries 0-5 (n, mean, M):
+// mean = p + S1/n, M = S2 - S1^2/n.
+__device__ __forceinline__ void sum3_tree(double& c, double& s1, double& s2, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();  // sh may still be read by a previous call
+  if (lane == 0) { sh[3 * w] = c; sh[3 * w + 1] = s1; sh[3 * w + 2] = s2; }
+  __syncthreads();
+  c = s1 = s2 = 0.0;
+  for (int i = 0; i < nw; ++i) { c += sh[3 * i]; s1 += sh[3 * i + 1]; s2 += sh[3 * i + 2]; }
+}
+
+template <typename IT, int FK, int U>
+__global__ void __launch_bounds__(256)
+k_moments_plane(int64_t nblocks, const void* __restrict__ maxima, const IT* __restrict__ dc,
+                double* __restrict__ ws, double* __restrict__ record) {
+  constexpr int RUN = 16;
+  constexpr int DCV = RUN * (int)sizeof(IT) / 16;                        // dc vectors per run
+  constexpr int MXV = FK == BZ_F64 ? 8 : (FK == BZ_F32 ? 4 : 2);        // maxima vectors per run
+  const int64_t nruns = nblocks / RUN;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const double p = nblocks > 0 ? (double)dc[0] * load_kind<FK>(maxima, 0) : 0.0;  // pivot
+  double c = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r0 < nruns; r0 += nth * U) {
+    uint4 dv[U][DCV], mv[U][MXV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = r0 + u * nth;
+      const bool ok = r < nruns;
+      const uint4* dsrc = reinterpret_cast<const uint4*>(dc + r * RUN);
+      const uint4* msrc = reinterpret_cast<const uint4*>(
+          reinterpret_cast<const unsigned char*>(maxima) + r * (16 * MXV));
+#pragma unroll
+      for (int k = 0; k < DCV; ++k) dv[u][k] = ok ? __ldcs(dsrc + k) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < MXV; ++k) mv[u][k] = ok ? __ldcs(msrc + k) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (r0 + u * nth >= nruns) break;
+      const IT* f0 = reinterpret_cast<const IT*>(dv[u]);
+      double a1 = 0.0, a2 = 0.0;  // two chains per run (latency)
+#pragma unroll
+      for (int e = 0; e < RUN; ++e) {
+        double n;
+        if constexpr (FK == BZ_F64) n = reinterpret_cast<const double*>(mv[u])[e];
+        else if constexpr (FK == BZ_F32) n = (double)reinterpret_cast<const float*>(mv[u])[e];
+        else n = load_kind<FK>(mv[u], e);
+        const double x = __fma_rn((double)f0[e], n, -p);  // F0*N is exact in f64 only for
+        a1 += x;                                          // narrow kinds; fma keeps one rounding
+        a2 = __fma_rn(x, x, a2);
+      }
+      c += (double)RUN;
+      s1 += a1;
+      s2 += a2;
+    }
+  }
+  // tail blocks (fewer than one run)
+  for (int64_t b = nruns * RUN + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblocks;
+       b += nth) {
+    const double x = __fma_rn((double)dc[b], load_kind<FK>(maxima, b), -p);
+    c += 1.0;
+    s1 += x;
+    s2 = __fma_rn(x, x, s2);
+  }
+  __shared__ double sh[3 * 32];
+  __shared__ bool last;
+  sum3_tree(c, s1, s2, sh);
+  unsigned* counter = reinterpret_cast<unsigned*>(ws);
+  double* parts = ws + 2;
+  if (threadIdx.x == 0) {
+    parts[3 * blockIdx.x] = c;
+    parts[3 * blockIdx.x + 1] = s1;
+    parts[3 * blockIdx.x + 2] = s2;
+    last = ticket_arrive(counter) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  c = s1 = s2 = 0.0;
+  const int per = (gridDim.x + blockDim.x - 1) / blockDim.x;
+  for (int i = threadIdx.x * per; i < min((int)gridDim.x, (int)(threadIdx.x + 1) * per); ++i) {
+    c += __ldcg(parts + 3 * i);
+    s1 += __ldcg(parts + 3 * i + 1);
+    s2 += __ldcg(parts + 3 * i + 2);
+  }
+  sum3_tree(c, s1, s2, sh);
+  if (threadIdx.x == 0) {
+    const double ma = c > 0.0 ? p + s1 / c : 0.0;
+    const double m2 = c > 0.0 ? s2 - s1 * (s1 / c) : 0.0;
+    record[0] = c;
+    record[1] = ma; record[2] = ma;
+    record[3] = m2; record[4] = m2; record[5] = m2;
+    for (int i = 6; i < BZ_RECORD_DOUBLES - 1; ++i) record[i] = 0.0;
+    record_complete(record);
+    *counter = 0u;  // re-arm
+  }
 }
 
 // ---------------------------------------------------------------- launch --
@@ -608,9 +719,7 @@ size_t moments_workspace(const Geo& g) {
 
 template <typename K>
 static int persistent_grid(K kern, int threads, size_t smem, int64_t work_ctas) {
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
-  occ = std::max(1, std::min(occ, kMaxCTAs / kSMs));
+  const int occ = std::max(1, std::min(occupancy((const void*)kern, threads, smem), kMaxCTAs / kSMs));
   return (int)std::max<int64_t>(1, std::min<int64_t>(work_ctas, (int64_t)kSMs * occ));
 }
 
@@ -628,8 +737,8 @@ static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const v
     constexpr int U = 8;
     auto kern = k_moments_dc<IT, U, PAIR>;
     const int grid = persistent_grid(kern, 256, 0, (B + 256 * U - 1) / (256 * U));
-    kern<<<grid, 256, 0, s>>>(B, kept, ga.float_kind, gb.float_kind, a_max, (const IT*)a_idx,
-                              b_max, (const IT*)b_idx, ws, record);
+    kern<<<grid, 256, 0, s>>>(B, (int64_t)kept, ga.float_kind, gb.float_kind, a_max,
+                              (const IT*)a_idx, b_max, (const IT*)b_idx, ws, record);
     return check_launch("moments_dc");
   }
   const uintptr_t base = (uintptr_t)a_idx | (PAIR ? (uintptr_t)b_idx : 0);
@@ -668,8 +777,7 @@ static int launch_typed(const Geo& ga, const Geo& gb, const void* a_max, const v
   const size_t smem = 2 * (((tile + 32 + 15) / 16) * 16);
   if (smem > 200 * 1024) { set_error("moments: kept block too large to stage"); return BZ_E_UNSUPPORTED; }
   auto kern = k_moments_staged<IT, PAIR>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = persistent_grid(kern, 256, smem, (B + 255) / 256);
+  const int grid = persistent_grid(kern, 256, smem, (B + 255) / 256);  // sets the smem limit
   kern<<<grid, 256, smem, s>>>(B, kept, kf, ga.float_kind, gb.float_kind, a_max,
                                (const IT*)a_idx, b_max, (const IT*)b_idx, ws, record);
   return check_launch("moments_staged");
@@ -683,6 +791,50 @@ static int launch_moments_t(const Geo& ga, const Geo& gb, const void* a_max, con
   double* w = (double*)ws;
   return pair ? launch_typed<IT, true>(ga, gb, a_max, a_idx, b_max, b_idx, dc_only, w, record, s)
               : launch_typed<IT, false>(ga, gb, a_max, a_idx, b_max, b_idx, dc_only, w, record, s);
+}
+
+// mean from the DC plane (k_moments_plane when the plane and maxima are
+// 16-byte aligned; otherwise the dc_only gather kernel with stride 1)
+template <typename IT>
+static int launch_plane_t(const Geo& g, const void* maxima, const void* dc, double* ws,
+                          double* record, cudaStream_t s) {
+  if (!(((uintptr_t)maxima | (uintptr_t)dc) & 15)) {
+    const int64_t runs = g.nblocks / 16;
+    constexpr int U = 2;
+#define BZ_PL(FKV)                                                                             \
+  {                                                                                            \
+    auto kern = k_moments_plane<IT, FKV, U>;                                                   \
+    const int grid = persistent_grid(kern, 256, 0, (runs + 256 * U - 1) / (256 * U));          \
+    kern<<<grid, 256, 0, s>>>(g.nblocks, maxima, (const IT*)dc, ws, record);                   \
+    return check_launch("moments_plane");                                                      \
+  }
+    switch (g.float_kind) {
+      case BZ_F64: { BZ_PL(BZ_F64) }
+      case BZ_F32: { BZ_PL(BZ_F32) }
+      case BZ_F16: { BZ_PL(BZ_F16) }
+      default: { BZ_PL(BZ_BF16) }
+    }
+#undef BZ_PL
+  }
+  constexpr int U = 8;
+  auto kern = k_moments_dc<IT, U, false>;
+  const int grid = persistent_grid(kern, 256, 0, (g.nblocks + 256 * U - 1) / (256 * U));
+  kern<<<grid, 256, 0, s>>>(g.nblocks, (int64_t)1, g.float_kind, g.float_kind, maxima,
+                            (const IT*)dc, maxima, (const IT*)dc, ws, record);
+  return check_launch("moments_plane");
+}
+
+int launch_moments_plane(const Geo& g, const void* maxima, const void* dc, double* record,
+                         void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (ws_bytes < moments_workspace(g)) { set_error("moments: workspace too small"); return BZ_E_WORKSPACE; }
+  if (!g.keeps_first || g.kept == 0) { set_error("moments_plane: mask drops the first coefficient"); return BZ_E_INVALID; }
+  double* w = (double*)ws;
+  switch (g.index_kind) {
+    case BZ_I8: return launch_plane_t<int8_t>(g, maxima, dc, w, record, s);
+    case BZ_I16: return launch_plane_t<int16_t>(g, maxima, dc, w, record, s);
+    case BZ_I32: return launch_plane_t<int32_t>(g, maxima, dc, w, record, s);
+    default: return launch_plane_t<int64_t>(g, maxima, dc, w, record, s);
+  }
 }
 
 int launch_moments(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,

@@ -66,6 +66,13 @@ __global__ void k_scale_maxima(const void* in, void* out, int fk, int64_t n, dou
     store_kind_rt(out, i, round_to_kind_rt(__dmul_rn(load_kind_rt(in, i, fk), ax), fk), fk);
 }
 
+// sign(x) applied to indices (x <= 0 or NaN): -F or 0 (ops.py:222)
+int launch_mul_scalar_indices(const Geo& g, const void* indices, double x, void* indices_out,
+                              cudaStream_t s) {
+  return launch_negate_mode(g.index_kind, indices, indices_out, g.nblocks * g.kept,
+                            x < 0 ? -1 : 0, s);
+}
+
 int launch_mul_scalar(const Geo& g, const void* maxima, const void* indices, double x,
                       void* maxima_out, void* indices_out, cudaStream_t s) {
   if (g.nblocks > 0) {

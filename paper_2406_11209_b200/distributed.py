@@ -75,13 +75,14 @@ class ShardedCompressedArray(CompressedArray):
 
     def __init__(self, local: CompressedArray, global_shape, group=None, record_fn=None):
         super().__init__(local.original_shape, local.settings, local.maxima, local.indices,
-                         _trusted=True)
+                         _trusted=True, dc=local.dc_plane)
         object.__setattr__(self, "global_shape", validate_shape(global_shape))
         object.__setattr__(self, "group", group)
         object.__setattr__(self, "_record_fn", record_fn or _device_record)
 
-    def _derive(self, maxima, indices):
-        local = CompressedArray(self.original_shape, self.settings, maxima, indices, _trusted=True)
+    def _derive(self, maxima, indices, dc=None):
+        local = CompressedArray(self.original_shape, self.settings, maxima, indices, _trusted=True,
+                                dc=dc)
         return ShardedCompressedArray(local, self.global_shape, self.group, self._record_fn)
 
     def _reduce_record(self, b, dc_only):
@@ -95,13 +96,14 @@ class ShardedCompressedArray(CompressedArray):
     @property
     def local(self) -> CompressedArray:
         return CompressedArray(self.original_shape, self.settings, self.maxima, self.indices,
-                               _trusted=True)
+                               _trusted=True, dc=self.dc_plane)
 
 
 def _device_record(a, b, dc_only):
-    plain_a = CompressedArray(a.original_shape, a.settings, a.maxima, a.indices, _trusted=True)
+    plain_a = CompressedArray(a.original_shape, a.settings, a.maxima, a.indices, _trusted=True,
+                              dc=a.dc_plane)
     plain_b = None if b is None else CompressedArray(b.original_shape, b.settings, b.maxima,
-                                                     b.indices, _trusted=True)
+                                                     b.indices, _trusted=True, dc=b.dc_plane)
     return moments_record(plain_a, plain_b, dc_only=dc_only)
 
 
@@ -122,7 +124,10 @@ def concat_shards(shards: list[CompressedArray], global_shape) -> CompressedArra
     s = shards[0].settings
     m = torch.cat([x.maxima.to(shards[0].device) for x in shards], dim=0)
     i = torch.cat([x.indices.to(shards[0].device) for x in shards], dim=0)
-    return CompressedArray(tuple(global_shape), s, m, i, _trusted=True)
+    dc = None
+    if all(x.dc_plane is not None for x in shards):
+        dc = torch.cat([x.dc_plane.to(shards[0].device) for x in shards], dim=0)
+    return CompressedArray(tuple(global_shape), s, m, i, _trusted=True, dc=dc)
 
 
 def expected_partition(global_shape, block_shape, world: int) -> list[tuple[int, int]]:

@@ -18,12 +18,13 @@ import ctypes
 import math
 import threading
 from dataclasses import dataclass
+from typing import NamedTuple
 
 import numpy as np
 import torch
 
 from . import _native
-from .codec import CompressedArray, workspace
+from .codec import CompressedArray, new_dc_plane, workspace
 from .errors import (
     MaskExcludesMeanCoefficient,
     NegativeBaseWithFractionalWeight,
@@ -107,12 +108,19 @@ def _stream(a: CompressedArray) -> int:
     return _native.stream_handle(a.device)
 
 
-def _derive(a: CompressedArray, maxima, indices) -> CompressedArray:
-    """Result with a's shape/settings (and a's sharding, for sharded arrays)."""
+def _derive(a: CompressedArray, maxima, indices, dc=None) -> CompressedArray:
+    """Result with a's shape/settings (and a's sharding, for sharded arrays);
+    `dc` is the result's DC plane when the producing kernel wrote one."""
     hook = getattr(a, "_derive", None)
     if hook is not None:
-        return hook(maxima, indices)
-    return CompressedArray(a.original_shape, a.settings, maxima, indices, _trusted=True)
+        return hook(maxima, indices, dc)
+    out = CompressedArray(a.original_shape, a.settings, maxima, indices, _trusted=True, dc=dc)
+    object.__setattr__(out, "_lay", a.layout())
+    return out
+
+
+def _new_dc(a: CompressedArray):
+    return new_dc_plane(a.settings, a.maxima.shape, a.device)
 
 
 # ----------------------------------------------------------- elementwise ----
@@ -122,20 +130,26 @@ def negate(a: CompressedArray) -> CompressedArray:
     out = torch.empty_like(a.indices)
     _native.call("bz_negate", a.settings.index_kind.code, a.indices.data_ptr(), out.data_ptr(),
                  a.indices.numel(), _stream(a))
-    return _derive(a, a.maxima, out)
+    dc = None
+    if a.dc_plane is not None:
+        dc = torch.empty_like(a.dc_plane)
+        _native.call("bz_negate", a.settings.index_kind.code, a.dc_plane.data_ptr(),
+                     dc.data_ptr(), dc.numel(), _stream(a))
+    return _derive(a, a.maxima, out, dc)
 
 
 def _add(a: CompressedArray, b: CompressedArray, subtract: int) -> CompressedArray:
     _check_compatible(a, b, index_kind=True)
     out_max = torch.empty_like(a.maxima)
     out_idx = torch.empty_like(a.indices)
+    dc = _new_dc(a)
     La, Lb = a.layout(), b.layout()
     bi = b.indices if b.device == a.device else b.indices.to(a.device)
     bm = b.maxima if b.device == a.device else b.maxima.to(a.device)
     _native.call("bz_add", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
                  a.indices.data_ptr(), bm.data_ptr(), bi.data_ptr(), subtract,
-                 out_max.data_ptr(), out_idx.data_ptr(), _stream(a))
-    return _derive(a, out_max, out_idx)
+                 out_max.data_ptr(), out_idx.data_ptr(), _native.ptr(dc), _stream(a))
+    return _derive(a, out_max, out_idx, dc)
 
 
 @_native.on_device
@@ -157,10 +171,11 @@ def add_scalar(a: CompressedArray, x: float) -> CompressedArray:
     shift = float(x) * a.settings.block_mean_scale
     out_max = torch.empty_like(a.maxima)
     out_idx = torch.empty_like(a.indices)
+    dc = _new_dc(a)
     L = a.layout()
     _native.call("bz_add_scalar", ctypes.byref(L), a.maxima.data_ptr(), a.indices.data_ptr(),
-                 shift, out_max.data_ptr(), out_idx.data_ptr(), _stream(a))
-    return _derive(a, out_max, out_idx)
+                 shift, out_max.data_ptr(), out_idx.data_ptr(), _native.ptr(dc), _stream(a))
+    return _derive(a, out_max, out_idx, dc)
 
 
 @_native.on_device
@@ -169,16 +184,21 @@ def mul_scalar(a: CompressedArray, x: float) -> CompressedArray:
     x = float(x)
     out_max = torch.empty_like(a.maxima)
     out_idx = None if x > 0 else torch.empty_like(a.indices)
+    dc_in = a.dc_plane
+    dc_out = None if (x > 0 or dc_in is None) else torch.empty_like(dc_in)
     L = a.layout()
-    _native.call("bz_mul_scalar", ctypes.byref(L), a.maxima.data_ptr(), a.indices.data_ptr(), x,
-                 out_max.data_ptr(), None if out_idx is None else out_idx.data_ptr(), _stream(a))
-    return _derive(a, out_max, a.indices if out_idx is None else out_idx)
+    _native.call("bz_mul_scalar", ctypes.byref(L), a.maxima.data_ptr(), a.indices.data_ptr(),
+                 _native.ptr(dc_in), x, out_max.data_ptr(), _native.ptr(out_idx),
+                 _native.ptr(dc_out), _stream(a))
+    return _derive(a, out_max, a.indices if out_idx is None else out_idx,
+                   dc_in if x > 0 else dc_out)
 
 
 # ------------------------------------------------------------ reductions ----
-@dataclass(frozen=True)
-class Record:
-    """Partial sums of one array / shard (include/bzc_b200.h, bz_moments)."""
+class Record(NamedTuple):
+    """Partial sums of one array / shard (include/bzc_b200.h, bz_moments).
+    A named tuple: immutable, and built without per-field __setattr__ (this
+    sits on the host path of every scalar reduction)."""
 
     n: float
     mean_a: float
@@ -192,8 +212,7 @@ class Record:
 
     @classmethod
     def from_array(cls, v) -> "Record":
-        v = [float(x) for x in np.asarray(v, dtype=np.float64).reshape(-1)[:9]]
-        return cls(*v)
+        return cls._make(np.asarray(v, dtype=np.float64).reshape(-1)[:9].tolist())
 
     def as_array(self) -> np.ndarray:
         return np.array([self.n, self.mean_a, self.mean_b, self.m_ab, self.m_aa, self.m_bb,
@@ -238,7 +257,7 @@ def _reduce_workspace(dev: torch.device, La) -> torch.Tensor:
     if not _MOMENTS_WS_BYTES:  # the size depends on no layout field
         _MOMENTS_WS_BYTES.append(int(_native.query("bz_moments_workspace", ctypes.byref(La))))
     nbytes = _MOMENTS_WS_BYTES[0]
-    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    key = (dev.index, _native.stream_handle(dev))
     ws = _REDUCE_WS.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=dev)
@@ -278,6 +297,15 @@ def moments_record(a: CompressedArray, b: CompressedArray | None = None, *,
 
             Lb = _layout(b.settings, b.original_shape, dev, index_kind=wide)
     ws = _reduce_workspace(dev, La)
+    if dc_only == 1 and not pair and getattr(a, "_dc", None) is not None:
+        # mean: the contiguous DC plane instead of a stride-K gather
+        try:
+            _native.call("bz_moments_dc", ctypes.byref(La), a.maxima.data_ptr(),
+                         a._dc.data_ptr(), rec.data_ptr(), ws.data_ptr(), ws.numel(), _stream(a))
+        except _native.NativeError:
+            ws.zero_()
+            raise
+        return rec
     try:
         _native.call("bz_moments", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
                      a.indices.data_ptr(), bm.data_ptr() if pair else None,
@@ -300,7 +328,13 @@ def _host_record() -> torch.Tensor:
     if h is None:
         h = torch.empty(_native.RECORD_DOUBLES, dtype=torch.float64, pin_memory=True)
         _TLS.rec = h
+        _TLS.rec_np = h.numpy()
     return h
+
+
+def _host_record_np() -> np.ndarray:
+    _host_record()
+    return _TLS.rec_np
 
 
 def record_to_host(rec: torch.Tensor) -> np.ndarray:
@@ -310,8 +344,8 @@ def record_to_host(rec: torch.Tensor) -> np.ndarray:
     dev = rec.device
     h = _host_record()
     h.copy_(rec, non_blocking=True)
-    torch.cuda.current_stream(dev).synchronize()
-    return h.numpy().copy()
+    _native.sync_stream(dev)
+    return _host_record_np().copy()
 
 
 # dc_only = 2: plain sums over every kept position (no DC moments) -- all that
@@ -324,9 +358,19 @@ def _reduce(a, b=None, *, dc_only=False) -> Record:
     hook = getattr(a, "_reduce_record", None)
     if hook is not None:
         return hook(b, dc_only)
-    h = moments_record(a, b, dc_only=dc_only, out=_host_record())
-    torch.cuda.current_stream(a.device).synchronize()
-    return Record.from_array(h.numpy())
+    h = _host_record()
+    hn = _host_record_np()
+    pair = b is not None and b is not a
+    if pair and b.settings.index_kind is not a.settings.index_kind:
+        moments_record(a, b, dc_only=dc_only, out=h)  # widened through a device copy
+        _native.sync_stream(a.device)
+    else:
+        # the kernel's last CTA writes the record straight into this pinned
+        # buffer, completion flag last: poll the flag (no stream round trip)
+        hn[_native.RECORD_DOUBLES - 1] = 0.0
+        moments_record(a, b, dc_only=dc_only, out=h)
+        _native.call("bz_wait_record", h.data_ptr(), _stream(a))
+    return Record._make(hn[:9].tolist())
 
 
 def _radius(a) -> float:
@@ -472,7 +516,7 @@ def _subtract_l2_sq(a: CompressedArray, b: CompressedArray, out: torch.Tensor) -
     configuration (the caller composes subtract + l2_norm, also on the GPU)."""
     _check_compatible(a, b, index_kind=True)
     dev = a.device
-    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    key = (dev.index, _native.stream_handle(dev))
     nbytes = _native.query("bz_subtract_l2_workspace")
     ws = _SL2_WS.get(key)
     if ws is None or ws.numel() < nbytes:
@@ -577,7 +621,7 @@ def approx_wasserstein(a: CompressedArray, b: CompressedArray,
     dev = a.device
     La, Lb = a.layout(), b.layout()
     nbytes = _native.query("bz_wasserstein_workspace", ctypes.byref(La))
-    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    key = (dev.index, _native.stream_handle(dev))
     ws = _WS_W.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)

@@ -214,7 +214,7 @@ def test_c_abi_rejects_mismatched_layouts(bz, S, rng):
     lib = _native.load_library()
     rc = lib.bz_add(ctypes.byref(La), ctypes.byref(Lc), a.maxima.data_ptr(), a.indices.data_ptr(),
                     c.maxima.data_ptr(), c.indices.data_ptr(), 0, out_m.data_ptr(),
-                    out_i.data_ptr(), _native.stream_handle())
+                    out_i.data_ptr(), None, _native.stream_handle())
     assert rc != 0 and b"block counts differ" in lib.bz_last_error()
     rc = lib.bz_moments(ctypes.byref(La), ctypes.byref(Lc), a.maxima.data_ptr(),
                         a.indices.data_ptr(), c.maxima.data_ptr(), c.indices.data_ptr(), 1, 0,

@@ -46,6 +46,11 @@ def main(name):
         print(f"  kernel l2 (events)      {timeit(lambda: ops.moments_record(ca), 50) * 1e3:8.1f} us")
         print(f"  kernel dc (events)      {timeit(lambda: ops.moments_record(ca, dc_only=True), 50) * 1e3:8.1f} us")
         print(f"  launch only (host)      {wall(lambda: ops.moments_record(ca)):8.1f} us")
+        tiny = torch.zeros(16, dtype=torch.int8, device="cuda")
+        st = torch.cuda.current_stream()
+        print(f"  bare stream sync        {wall(lambda: st.synchronize()):8.1f} us")
+        print(f"  tiny launch + sync      {wall(lambda: (bz._native.call('bz_negate', 1, tiny.data_ptr(), tiny.data_ptr(), 16, st.cuda_stream), st.synchronize())):8.1f} us")
+        print(f"  moments + sync          {wall(lambda: (ops.moments_record(ca, dc_only=2), st.synchronize())):8.1f} us")
         print(f"  record_to_host          {wall(lambda: ops.record_to_host(rec)):8.1f} us")
         print(f"  l2_norm (public)        {wall(lambda: bz.l2_norm(ca)):8.1f} us")
         print(f"  mean (public)           {wall(lambda: bz.mean(ca)):8.1f} us")
