@@ -342,7 +342,6 @@ k_dct4_compress_tma(const __grid_constant__ CUtensorMap xmap, const FastParams p
   const uint32_t ebar0 = bar0 + 8 * STAGES;                      // empty[s]
   const int t = threadIdx.x;
   const int lane = t & 31, w = t >> 5;
-  const int64_t tpr = f.grid[3] / TB;  // tiles per row of blocks
   const int64_t ntiles = f.nblocks / TB;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -362,14 +361,12 @@ k_dct4_compress_tma(const __grid_constant__ CUtensorMap xmap, const FastParams p
         const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
         if (it >= STAGES) tma::mbar_wait(ebar0 + 8 * s, ph ^ 1u);
         tma::mbar_arrive_expect_tx(bar0 + 8 * s, STAGE_BYTES);
-        int64_t q = tile / tpr;
-        const int64_t r3 = tile - q * tpr;
-        const int64_t g2 = q % f.grid[2];
-        q /= f.grid[2];
-        const int64_t g1 = q % f.grid[1];
-        const int64_t g0 = q / f.grid[1];
+        // the tile's first block: magic-number divisions (a 64-bit division
+        // is a ~70-instruction routine on this single issuing thread)
+        int64_t gc[4];
+        block_coords<4>(f, tile * TB, gc);
         const uint32_t dst = stage0 + s * STAGE_BYTES;
-        const int c3 = (int)(r3 * 64), c2 = (int)(g2 * 4), c1 = (int)(g1 * 4), c0 = (int)(g0 * 4);
+        const int c3 = (int)(gc[3] * 4), c2 = (int)(gc[2] * 4), c1 = (int)(gc[1] * 4), c0 = (int)(gc[0] * 4);
         tma::load_4d(dst, &xmap, bar0 + 8 * s, c3, c2, c1, c0);
         tma::load_4d(dst + BOX_BYTES, &xmap, bar0 + 8 * s, c3 + 32, c2, c1, c0);
       }

@@ -68,7 +68,10 @@ __device__ __forceinline__ Rec rec_shfl(const Rec& x, int o) {
   return y;
 }
 
-// pivot-shifted per-thread accumulator (no divisions on the per-block path)
+// Pivot-shifted accumulator (no divisions on the per-block path).  Every
+// thread of a CTA shifts the DC values by the same pivots (the DC values of
+// one block of the CTA, set_pivot), so the threads' partials of a CTA are
+// plain sums that merge by addition; CTA records merge with Chan's formulas.
 struct MomState {
   double cnt = 0, pa = 0, pb = 0, sa = 0, sb = 0, sab = 0, saa = 0, sbb = 0;
   double Sab = 0, Saa = 0, Sbb = 0;
@@ -84,13 +87,11 @@ struct MomState {
     }
     if (dc) {
       const double dca = fa0 * na;
-      if (cnt == 0.0) pa = dca;
       const double xa = dca - pa;
       sa += xa;
       saa = __fma_rn(xa, xa, saa);
       if (PAIR) {
         const double dcb = fb0 * nb;
-        if (cnt == 0.0) pb = dcb;
         const double xb = dcb - pb;
         sb += xb;
         sab = __fma_rn(xa, xb, sab);
@@ -114,13 +115,11 @@ struct MomState {
   __device__ __forceinline__ void add_dc(double fa0, double fb0, double na, double nb, bool dc) {
     if (dc) {
       const double dca = fa0 * na;
-      if (cnt == 0.0) pa = dca;
       const double xa = dca - pa;
       sa += xa;
       saa = __fma_rn(xa, xa, saa);
       if (PAIR) {
         const double dcb = fb0 * nb;
-        if (cnt == 0.0) pb = dcb;
         const double xb = dcb - pb;
         sb += xb;
         sab = __fma_rn(xa, xb, sab);
@@ -128,6 +127,11 @@ struct MomState {
       }
     }
     cnt += 1.0;
+  }
+
+  __device__ __forceinline__ void set_pivot(double a, double b) {
+    pa = isfinite(a) ? a : 0.0;  // a non-finite pivot would poison every
+    pb = isfinite(b) ? b : 0.0;  // difference; 0 keeps the reference's propagation
   }
 
   __device__ __forceinline__ Rec record(bool dc) const {
@@ -176,17 +180,45 @@ __device__ __forceinline__ void store_rec(double* dst, const Rec& t) {
   dst[5] = t.Mbb; dst[6] = t.Sab; dst[7] = t.Saa; dst[8] = t.Sbb;
 }
 
-// Every CTA stores its record; the last CTA to finish (atomic ticket) merges
-// all of them in CTA order -- deterministic -- writes the final record and
-// re-arms the ticket counter.  ws layout: [counter (16 B)][CTA records].
-__device__ __forceinline__ void finish(Rec r, double* __restrict__ ws, int pair,
-                                       double* __restrict__ record) {
+// Additive tree of N doubles over a CTA (fixed order: deterministic); the
+// result is valid in every thread.
+template <int N>
+__device__ __forceinline__ void sum_tree(double (&v)[N], double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();  // sh may still be read by a previous call
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < N; ++k) sh[N * w + k] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = 0.0;
+  for (int i = 0; i < nw; ++i)
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] += sh[N * i + k];
+}
+
+// The CTA's threads share one pivot: their partials add up (one additive
+// tree); thread 0 turns the CTA's sums into a record and stores it; the last
+// CTA to arrive (acquire-release ticket) Chan-merges all CTA records in CTA
+// order -- deterministic -- writes the final record and re-arms the ticket.
+// ws layout: [counter (16 B)][CTA records].
+__device__ __forceinline__ void finish(const MomState& st, bool dc, double* __restrict__ ws,
+                                       int pair, double* __restrict__ record) {
   unsigned int* counter = reinterpret_cast<unsigned int*>(ws);
   double* recs = ws + 2;
-  Rec t = cta_tree(r);
+  __shared__ double sh[9 * 32];
   __shared__ bool last;
+  double v[9] = {st.cnt, st.sa, st.sb, st.sab, st.saa, st.sbb, st.Sab, st.Saa, st.Sbb};
+  sum_tree<9>(v, sh);
   if (threadIdx.x == 0) {
-    store_rec(recs + blockIdx.x * BZ_RECORD_DOUBLES, t);
+    MomState c = st;
+    c.cnt = v[0]; c.sa = v[1]; c.sb = v[2]; c.sab = v[3]; c.saa = v[4]; c.sbb = v[5];
+    c.Sab = v[6]; c.Saa = v[7]; c.Sbb = v[8];
+    store_rec(recs + blockIdx.x * BZ_RECORD_DOUBLES, c.record(dc));
     last = ticket_arrive(counter) == gridDim.x - 1;
   }
   __syncthreads();
@@ -205,6 +237,45 @@ __device__ __forceinline__ void finish(Rec r, double* __restrict__ ws, int pair,
     for (int i = 9; i < BZ_RECORD_DOUBLES - 1; ++i) record[i] = 0.0;
     record_complete(record);
     *counter = 0u;  // re-arm for the next launch on this workspace
+  }
+}
+
+// "Sums" mode (dot / l2, no DC moments): the partials are plain sums
+// (block count, S_ab, S_aa, S_bb), merged by addition in a fixed order --
+// the reference's own arithmetic (np.dot over the chunks), and a far shorter
+// tail than the Chan merge of full records.
+__device__ __forceinline__ void finish_sums(double n, double sab, double saa, double sbb,
+                                            double* __restrict__ ws, int pair,
+                                            double* __restrict__ record) {
+  unsigned* counter = reinterpret_cast<unsigned*>(ws);
+  double* parts = ws + 2;
+  __shared__ double sh[4 * 32];
+  __shared__ bool last;
+  double v[4] = {n, sab, saa, sbb};
+  sum_tree<4>(v, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) parts[4 * blockIdx.x + k] = v[k];
+    last = ticket_arrive(counter) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = 0.0;
+  const int per = (gridDim.x + blockDim.x - 1) / blockDim.x;
+  for (int i = threadIdx.x * per; i < min((int)gridDim.x, (int)(threadIdx.x + 1) * per); ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] += __ldcg(parts + 4 * i + k);
+  sum_tree<4>(v, sh);
+  if (threadIdx.x == 0) {
+    record[0] = v[0];
+    for (int i = 1; i < 6; ++i) record[i] = 0.0;
+    record[6] = pair ? v[1] : v[2];
+    record[7] = v[2];
+    record[8] = pair ? v[3] : v[2];
+    for (int i = 9; i < BZ_RECORD_DOUBLES - 1; ++i) record[i] = 0.0;
+    record_complete(record);
+    *counter = 0u;  // re-arm
   }
 }
 
@@ -389,6 +460,11 @@ k_moments_stream(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool dc = DC && keeps_first != 0;
   MomState st;
+  if (dc && nblocks > 0) {  // the CTA's pivots: the DC values of one of its blocks
+    const int64_t pb_ = blockIdx.x % nblocks;
+    const double pva = (double)a_idx[pb_ * kept] * (double)ld_max<FK>(a_max, pb_, fk_a);
+    st.set_pivot(pva, PAIR ? (double)b_idx[pb_ * kept] * (double)ld_max<FK>(b_max, pb_, fk_b) : pva);
+  }
   const unsigned char* ca = reinterpret_cast<const unsigned char*>(a_idx);
   const unsigned char* cb = reinterpret_cast<const unsigned char*>(b_idx);
   const int64_t qs = (nth * V) / kept;
@@ -483,7 +559,8 @@ k_moments_stream(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
                                (double)sprod<IT>(y, y), na, nb);
     }
   }
-  finish(st.record(dc), ws, PAIR, record);
+  if constexpr (DC) finish(st, dc, ws, PAIR, record);
+  else finish_sums(st.cnt, st.Sab, st.Saa, st.Sbb, ws, PAIR, record);
 }
 
 // ---------------------------------- unaligned blocks: staged, one per thread --
@@ -500,6 +577,11 @@ k_moments_staged(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
   unsigned char* sb = smem_raw + ((tile_bytes + 32 + 15) / 16) * 16;
   const bool dc = keeps_first != 0;
   MomState st;
+  if (dc && nblocks > 0 && kept > 0) {  // the CTA's pivots (see MomState)
+    const int64_t pb_ = blockIdx.x % nblocks;
+    const double pva = (double)a_idx[pb_ * kept] * load_kind_rt(a_max, pb_, fk_a);
+    st.set_pivot(pva, PAIR ? (double)b_idx[pb_ * kept] * load_kind_rt(b_max, pb_, fk_b) : pva);
+  }
   const int64_t ntiles = (nblocks + T - 1) / T;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t b0 = tile * T;
@@ -565,7 +647,7 @@ k_moments_staged(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
     }
     __syncthreads();
   }
-  finish(st.record(dc), ws, PAIR, record);
+  finish(st, dc, ws, PAIR, record);
 }
 
 // ------------------------------------------------- first coefficients only --
@@ -578,6 +660,11 @@ k_moments_dc(int64_t nblocks, int64_t kept, int fk_a, int fk_b, const void* __re
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   MomState st;
+  if (nblocks > 0) {  // the CTA's pivots (see MomState)
+    const int64_t pb_ = blockIdx.x % nblocks;
+    const double pva = (double)a_idx[pb_ * kept] * load_kind_rt(a_max, pb_, fk_a);
+    st.set_pivot(pva, PAIR ? (double)b_idx[pb_ * kept] * load_kind_rt(b_max, pb_, fk_b) : pva);
+  }
   for (int64_t bb = tid; bb < nblocks; bb += nth * U) {
     double fa[U], fb[U], na[U], nb[U];
 #pragma unroll
@@ -593,7 +680,7 @@ k_moments_dc(int64_t nblocks, int64_t kept, int fk_a, int fk_b, const void* __re
     for (int u = 0; u < U; ++u)
       if (bb + u * nth < nblocks) st.add_block<PAIR>(0, 0, 0, fa[u], fb[u], na[u], nb[u], true);
   }
-  finish(st.record(true), ws, PAIR, record);
+  finish(st, true, ws, PAIR, record);
 }
 
 // DC plane (mean, ops.py:244-257): each thread owns runs of 16 consecutive

@@ -94,6 +94,10 @@ def run(name):
     rec_("decompress_fk", lambda: timeit(lambda: bz.decompress(ca, kind)), comp_bytes + n * kind.itemsize)
     rec_("l2_record", lambda: timeit(lambda: bz.ops.moments_record(ca, dc_only=2)), comp_bytes)
     rec_("dot_record", lambda: timeit(lambda: bz.ops.moments_record(ca, cb, dc_only=2)), 2 * comp_bytes, 2 * inb)
+    if s.mask.keeps_first:
+        rec_("cov_record", lambda: timeit(lambda: bz.ops.moments_record(ca, cb)), 2 * comp_bytes, 2 * inb)
+        rec_("mean_record", lambda: timeit(lambda: bz.ops.moments_record(ca, dc_only=1)),
+             B * (s.index_kind.itemsize + kind.itemsize))
     rec_("add", lambda: timeit(lambda: bz.add(ca, cb)), 3 * comp_bytes, 2 * inb)
     rec_("negate", lambda: timeit(lambda: bz.negate(ca)), 2 * B * K * s.index_kind.itemsize)
     rec_("l2_norm(api)", lambda: timeit(lambda: bz.l2_norm(ca)), comp_bytes)
