@@ -65,6 +65,10 @@ __device__ __forceinline__ Dct4K dct4_consts(const double (&H)[64]) {
   return Dct4K{2.0 * H[1], 2.0 * H[3]};
 }
 constexpr double kUnscale = 0.0625;  // 1 / 2^4
+struct FastGeoRef {
+  int32_t full_mask;
+  const int32_t* rank;
+};
 
 // forward line (stride S), times 2: 2 C[k] = 2 sum_n x[n] H[n][k]
 template <int S>
@@ -92,38 +96,38 @@ __device__ __forceinline__ void idct4(double* v, const Dct4K& K) {
 
 // Everything after a warp's two blocks are in registers (v[a0*4 + a3] at
 // (a1, a2) = (i1, i2) of block b): axes 0 and 3, the warp-local exchange,
-// axes 1 and 2, maximum, binning, staging and the contiguous copy-out of
-// the pair's kept indices (blocks b0, b0 + 1).  Shared by the cp.async and
+// axes 1 and 2, maximum and binning into the warp's output staging (byte
+// addresses ra[q] + OFF; dropped coefficients go to a scratch byte).  The
+// caller copies the staged kept indices out.  Shared by the cp.async and
 // the TMA kernels.
 struct Ctx4 {
   int lane, bs, o;
-  int K;
-  int64_t nblocks;
   d4::Dct4K KC;
   double* wbase;  // phase A write base of this lane
   double* rbase;  // phase B read base of this lane
-  int8_t* stg;    // the warp's output staging (2 x SS bytes)
-  int8_t* sbase;  // this block's staging run (stg + bs*K)
 };
 
-template <int FK>
-__device__ __forceinline__ void dct4_compress_pair(double (&v)[16], const int16_t (&rk)[16],
-                                                   const Ctx4& cx, int64_t b0,
-                                                   int64_t b, bool valid,
-                                                   void* __restrict__ maxima,
-                                                   int8_t* __restrict__ indices,
-                                                   int32_t* __restrict__ list,
-                                                   int32_t* __restrict__ count,
-                                                   int8_t* __restrict__ dc) {
+__device__ __forceinline__ void sts_u8(uint32_t addr, unsigned v) {
+  asm volatile("st.shared.u8 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+
+// 1.5 * 2^28 + 1/2 + 2^-24 (exact: 53 significant bits): fma(c, r/N, kMagicY)
+// leaves y = RN(v * 2^24) + 2^23 + 1 in the low word, v = c r / N -- the
+// index is y's top byte unless the 24-bit fraction y & 0xffffff is <= 2
+// (within one unit of a rounding half; bz_dct8.cu)
+constexpr double kMagicY = 1.5 * 268435456.0 + 0.5 + 0x1p-24;
+
+template <int FK, int OFF>
+__device__ __forceinline__ void dct4_pair_core(double (&v)[16], const uint32_t (&ra)[16],
+                                               const Ctx4& cx, int64_t b, bool valid,
+                                               void* __restrict__ maxima,
+                                               int32_t* __restrict__ list,
+                                               int32_t* __restrict__ count) {
   using namespace d4;
-  const int lane = cx.lane, bs = cx.bs, o = cx.o, K = cx.K;
+  const int bs = cx.bs, o = cx.o;
   const Dct4K KC = cx.KC;
   double* wbase = cx.wbase;
   double* rbase = cx.rbase;
-  int8_t* stg = cx.stg;
-  int8_t* sbase = cx.sbase;
-  constexpr int ZS = 2 * BS;
-  struct { int64_t nblocks; } f{cx.nblocks};
 #pragma unroll
   for (int a3 = 0; a3 < 4; ++a3) fdct4<4>(v + a3, KC);  // axis 0
 #pragma unroll
@@ -147,13 +151,12 @@ __device__ __forceinline__ void dct4_compress_pair(double (&v)[16], const int16_
   // signed winners, magnitudes compared through the |.| modifier (no
   // instruction materialises |v|)
   // (chains start from real elements, not 0.0: see bz_dct8.cu)
-  double m0 = v[0], m1 = v[1];
+  double m4[4] = {v[0], v[1], v[2], v[3]};
 #pragma unroll
-  for (int q = 2; q < 16; q += 2) {
-    m0 = fabs(v[q]) > fabs(m0) ? v[q] : m0;
-    m1 = fabs(v[q + 1]) > fabs(m1) ? v[q + 1] : m1;
-  }
-  double m = fabs(m1) > fabs(m0) ? fabs(m1) : fabs(m0);
+  for (int q = 4; q < 16; ++q) m4[q & 3] = fabs(v[q]) > fabs(m4[q & 3]) ? v[q] : m4[q & 3];
+  double m = fabs(m4[1]) > fabs(m4[0]) ? fabs(m4[1]) : fabs(m4[0]);
+  const double m23 = fabs(m4[3]) > fabs(m4[2]) ? fabs(m4[3]) : fabs(m4[2]);
+  m = m23 > m ? m23 : m;
 #pragma unroll
   for (int sft = 8; sft > 0; sft >>= 1) {
     const double a = __shfl_xor_sync(0xffffffffu, m, sft);
@@ -166,38 +169,48 @@ __device__ __forceinline__ void dct4_compress_pair(double (&v)[16], const int16_
   bool bad = !bc.fast || !(mx < 1.7976931348623157e308) ||
              round_to_kind<FK>(mx * (1.0 - kDeltaRel)) != round_to_kind<FK>(mx * (1.0 + kDeltaRel));
 
-  // ---- bin the kept coefficients (24-bit fixed point, as bz_dct8.cu) into
-  // the warp's staging area at slot bs*K + rank (dropped ones: a scratch slot)
-  unsigned zmin = 0xffffffffu;
+  // ---- bin into the staging bytes (24-bit fixed point, bz_dct8.cu).  The
+  // near-half test runs over all 16 coefficients: a dropped one can only
+  // send its block to the exact fix-up needlessly (probability ~2^-22)
+  unsigned z4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
-    const int fx = __double2loint(__fma_rn(v[q], R16, 1.5 * 268435456.0));
-    const unsigned y1 = (unsigned)fx + (1u << 23) + 1u;
-    zmin = min(zmin, rk[q] != ZS - bs * K ? (y1 & 0xffffffu) : 0xffffffffu);  // kept only
-    sbase[rk[q]] = (int8_t)(y1 >> 24);
+    const unsigned y1 = (unsigned)__double2loint(__fma_rn(v[q], R16, kMagicY));
+    z4[q & 3] = min(z4[q & 3], y1 & 0xffffffu);
+    sts_u8(ra[q] + OFF, y1 >> 24);
   }
-  bad = bad || zmin <= 2u;
+  bad = bad || min(min(z4[0], z4[1]), min(z4[2], z4[3])) <= 2u;
   const unsigned badmask = __ballot_sync(0xffffffffu, bad && valid);
   if (valid && o == 0) {
     store_kind<FK>(maxima, b, n);
     if ((badmask >> (bs * 16)) & 0xffffu) list[atomicAdd(count, 1)] = (int32_t)b;
   }
-  __syncwarp();
-  // ---- the warp tile's kept indices: one contiguous run of nvalid * K bytes
-  {
-    const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
-    const int nbytes = nv * K;
-    int8_t* dst = indices + b0 * (int64_t)K;
-    // staged contiguously: one word per lane (and a second) when aligned
-    if ((((uintptr_t)dst | (uintptr_t)nbytes) & 3) == 0) {
-      const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
-      uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-      for (int i = lane; i < nbytes / 4; i += 32) __stcs(d32 + i, s32[i]);
-    } else {
-      for (int e2 = lane; e2 < nbytes; e2 += 32) dst[e2] = stg[e2];
-    }
-    // DC plane (passed only when the mask keeps position 0, rank 0)
-    if (dc && lane < nv) dc[b0 + lane] = stg[lane * K];
+}
+
+// staging byte addresses of this lane's 16 coefficients (k0 = o>>2,
+// k3 = o&3, k1, k2): block bs's kept run starts at stg + bs*K; a dropped
+// coefficient goes to the scratch byte stg + scratch
+__device__ __forceinline__ void dct4_stage_addrs(const d4::FastGeoRef& f, int o, int bs, int K,
+                                                 uint32_t stg, int scratch, uint32_t (&ra)[16]) {
+  const int k0 = o >> 2, k3 = o & 3;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int r_ = f.full_mask ? (k0 * 64 + q * 4 + k3) : f.rank[k0 * 64 + q * 4 + k3];
+    ra[q] = stg + (uint32_t)(r_ >= 0 ? bs * K + r_ : scratch);
+  }
+}
+
+// copy `nbytes` staged bytes to dst: 32-bit words when both are 4-byte
+// multiples; segment 2 (bytes [seg, nbytes)) comes from stg + hop + ...
+__device__ __forceinline__ void dct4_copy_out(const int8_t* stg, int seg, int hop, int nbytes,
+                                              int8_t* dst, int lane) {
+  if ((((uintptr_t)dst | (uintptr_t)nbytes | (uintptr_t)seg) & 3) == 0) {
+    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
+    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+    const int sw = seg / 4, hw = hop / 4;
+    for (int i = lane; i < nbytes / 4; i += 32) __stcs(d32 + i, s32[i < sw ? i : i + hw]);
+  } else {
+    for (int e = lane; e < nbytes; e += 32) dst[e] = stg[e < seg ? e : e + hop];
   }
 }
 
@@ -216,16 +229,8 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
   double* blk = reinterpret_cast<double*>(smem_raw) + (w * BPW + bs) * XS;
   const int K = f.kept;
   const Dct4K KC = dct4_consts(p.H);
-  // rank (output slot within the block) of this lane's 16 coefficients
-  // (k0 = o>>2, k3 = o&3, k1, k2); -1 when the mask drops it
-  const int k0 = o >> 2, k3 = o & 3;
-  int16_t rk[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int r_ = f.full_mask ? (k0 * 64 + q * 4 + k3) : f.rank[k0 * 64 + q * 4 + k3];
-    rk[q] = (int16_t)(r_ >= 0 ? r_ : 2 * BS - bs * K);  // dropped: the scratch slot
-  }
   const int i1 = o >> 2, i2 = o & 3;
+  const int k0 = o >> 2, k3 = o & 3;
   double* wbase = blk + xoff(0, i1, i2, 0);  // phase A: (a0, a3) at immediates
   double* rbase = blk + xoff(k0, 0, 0, k3);  // phase B: (a1, a2) at immediates
   const int64_t s0 = f.stride[0], s1 = f.stride[1], s2 = f.stride[2];
@@ -259,7 +264,9 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
   bool staged = prefetch(blockIdx.x * (int64_t)WPC + w);
   int8_t* stg = reinterpret_cast<int8_t*>(reinterpret_cast<double*>(smem_raw) + WPC * BPW * XS) +
                 w * BPW * SS;  // per-warp output staging, 2 x (256 + 16) bytes
-  const Ctx4 cx{lane, bs, o, K, f.nblocks, KC, wbase, rbase, stg, stg + bs * K};
+  uint32_t ra[16];
+  dct4_stage_addrs(FastGeoRef{f.full_mask, f.rank}, o, bs, K, tma::smem_u32(stg), 2 * BS, ra);
+  const Ctx4 cx{lane, bs, o, KC, wbase, rbase};
 
   for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += wstride) {
     const int64_t b = wt * BPW + bs;
@@ -296,7 +303,13 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
                                  ? (double)src[a0 * s0 + a3] : 0.0;
       }
     }
-    dct4_compress_pair<FK>(v, rk, cx, wt * BPW, b, valid, maxima, indices, list, count, dc);
+    dct4_pair_core<FK, 0>(v, ra, cx, b, valid, maxima, list, count);
+    __syncwarp();
+    // ---- the warp tile's kept indices: one contiguous run of nvalid * K bytes
+    const int64_t b0 = wt * BPW;
+    const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
+    dct4_copy_out(stg, nv * K, 0, nv * K, indices + b0 * (int64_t)K, lane);
+    if (dc && lane < nv) dc[b0 + lane] = stg[lane * K];  // DC plane (rank 0 = position 0)
     __syncwarp();  // staging and exchange area reused by the next tile
   }
 }
@@ -306,9 +319,12 @@ k_dct4_compress(const FastParams p, const float* __restrict__ x, void* __restric
 // f32 box = two TMA boxes of 4 x 4 x 4 x 32, 128-byte swizzled) stream
 // through a STAGES-deep ring of shared-memory buffers: warp 8 (one elected
 // lane) issues cp.async.bulk.tensor loads that complete on the stage's
-// `full` mbarrier; the 8 consumer warps (two blocks each, the lane layout
-// of k_dct4_compress) read their rows with conflict-free 16-byte loads,
-// release the stage on its `empty` mbarrier and run the shared pipeline.
+// `full` mbarrier.  The 8 consumer warps form two groups of 4 that take
+// alternate tiles; a warp handles 4 consecutive blocks of its tile as two
+// pairs (the lane layout of k_dct4_compress), reads their rows with
+// conflict-free 16-byte loads, releases the stage on its `empty` mbarrier
+// and writes the 4 blocks' kept indices as one contiguous run -- the
+// per-tile and copy-out bookkeeping is paid once per 4 blocks.
 // No per-thread address arithmetic for the dense side: a block's linear
 // index is tile * 16 + j; out-of-range rows of partial blocks (axes 0-2)
 // arrive zero-filled by the TMA unit.
@@ -316,11 +332,14 @@ namespace d4t {
 constexpr int NCW = 8;                  // consumer warps
 constexpr int NT = (NCW + 1) * 32;      // + producer warp
 constexpr int TB = 16;                  // blocks per tile
+constexpr int GROUPS = 2;               // consumer groups (alternate tiles)
 constexpr int STAGES = 4;
 constexpr int BOX_BYTES = 8192;         // 4 x 4 x 4 x 32 f32
 constexpr int STAGE_BYTES = 2 * BOX_BYTES;
+constexpr int PAIRB = 2 * d4::BS;       // staging bytes per pair (2 blocks of <= 256)
+constexpr int STGW = 2 * PAIRB + 16;    // staging bytes per warp (+ scratch)
 constexpr size_t kSmem = 1024 + (size_t)STAGES * STAGE_BYTES + (size_t)NCW * 2 * d4::XS * 8 +
-                         (size_t)NCW * 2 * d4::SS + 2 * STAGES * 8;
+                         (size_t)NCW * STGW + 2 * STAGES * 8;
 }  // namespace d4t
 
 template <int FK>
@@ -338,15 +357,15 @@ k_dct4_compress_tma(const __grid_constant__ CUtensorMap xmap, const FastParams p
   const uint32_t stage0 = tma::smem_u32(base);
   double* xch = reinterpret_cast<double*>(base + STAGES * STAGE_BYTES);
   int8_t* stg_all = reinterpret_cast<int8_t*>(xch + NCW * 2 * XS);
-  const uint32_t bar0 = tma::smem_u32(stg_all + NCW * 2 * SS);  // full[s] at bar0 + 8s
-  const uint32_t ebar0 = bar0 + 8 * STAGES;                      // empty[s]
+  const uint32_t bar0 = tma::smem_u32(stg_all + NCW * STGW);  // full[s] at bar0 + 8s
+  const uint32_t ebar0 = bar0 + 8 * STAGES;                   // empty[s]
   const int t = threadIdx.x;
   const int lane = t & 31, w = t >> 5;
   const int64_t ntiles = f.nblocks / TB;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tma::mbar_init(bar0 + 8 * s, 1);
-      tma::mbar_init(ebar0 + 8 * s, NCW);
+      tma::mbar_init(ebar0 + 8 * s, NCW / GROUPS);
     }
     tma::fence_mbar_init();
   }
@@ -376,44 +395,58 @@ k_dct4_compress_tma(const __grid_constant__ CUtensorMap xmap, const FastParams p
 
   // ---------------------------------------------------------------- consumers
   const int bs = lane >> 4, o = lane & 15;
+  const int grp = w / (NCW / GROUPS), wg = w % (NCW / GROUPS);
   double* blk = xch + (w * 2 + bs) * XS;
-  int8_t* stg = stg_all + w * 2 * SS;
+  int8_t* stg = stg_all + w * STGW;
   const int K = f.kept;
   const Dct4K KC = dct4_consts(p.H);
   const int k0 = o >> 2, k3 = o & 3;
-  int16_t rk[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int r_ = f.full_mask ? (k0 * 64 + q * 4 + k3) : f.rank[k0 * 64 + q * 4 + k3];
-    rk[q] = (int16_t)(r_ >= 0 ? r_ : 2 * BS - bs * K);  // dropped: the scratch slot
-  }
   const int i1 = o >> 2, i2 = o & 3;
-  const Ctx4 cx{lane, bs, o, K, f.nblocks, KC, blk + xoff(0, i1, i2, 0), blk + xoff(k0, 0, 0, k3),
-                stg, stg + bs * K};
-  const int j = 2 * w + bs;  // block within the tile
+  uint32_t ra[16];  // pair 0 at stg, pair 1 at stg + PAIRB, scratch at stg + 2 PAIRB
+  dct4_stage_addrs(FastGeoRef{f.full_mask, f.rank}, o, bs, K, tma::smem_u32(stg), 2 * PAIRB, ra);
+  const Ctx4 cx{lane, bs, o, KC, blk + xoff(0, i1, i2, 0), blk + xoff(k0, 0, 0, k3)};
   // row r = a0*16 + o of box j/8, 16-byte chunk j%8 swizzled by r%8 = o%8
-  const uint32_t rd0 = (uint32_t)((j >> 3) * BOX_BYTES + o * 128 + (((j & 7) ^ (o & 7)) << 4));
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  // (blocks j = 4 wg + bs (pair 0) and 4 wg + 2 + bs (pair 1) of the tile)
+  const int j0 = 4 * wg + bs, j1 = j0 + 2;
+  const uint32_t rd0 = (uint32_t)((j0 >> 3) * BOX_BYTES + o * 128 + (((j0 & 7) ^ (o & 7)) << 4));
+  const uint32_t rd1 = (uint32_t)((j1 >> 3) * BOX_BYTES + o * 128 + (((j1 & 7) ^ (o & 7)) << 4));
+  int it = grp;
+  for (int64_t tile = blockIdx.x + (int64_t)grp * gridDim.x; tile < ntiles;
+       tile += (int64_t)GROUPS * gridDim.x, it += GROUPS) {
     const int s = it % STAGES;
     const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
     tma::mbar_wait(bar0 + 8 * s, ph);
-    const uint32_t src = stage0 + s * STAGE_BYTES + rd0;
-    float4 r[4];
+    const uint32_t src = stage0 + s * STAGE_BYTES;
+    float4 r0[4], r1[4];
 #pragma unroll
-    for (int a0 = 0; a0 < 4; ++a0) r[a0] = tma::lds128f(src + a0 * 16 * 128);
-    __syncwarp();
-    if (lane == 0) tma::mbar_arrive(ebar0 + 8 * s);  // stage free for the producer
+    for (int a0 = 0; a0 < 4; ++a0) r0[a0] = tma::lds128f(src + rd0 + a0 * 16 * 128);
+    const int64_t b0 = tile * TB + 4 * wg;
     double v[16];
 #pragma unroll
     for (int a0 = 0; a0 < 4; ++a0) {
-      v[a0 * 4 + 0] = (double)r[a0].x;
-      v[a0 * 4 + 1] = (double)r[a0].y;
-      v[a0 * 4 + 2] = (double)r[a0].z;
-      v[a0 * 4 + 3] = (double)r[a0].w;
+      v[a0 * 4 + 0] = (double)r0[a0].x;
+      v[a0 * 4 + 1] = (double)r0[a0].y;
+      v[a0 * 4 + 2] = (double)r0[a0].z;
+      v[a0 * 4 + 3] = (double)r0[a0].w;
     }
-    const int64_t b0 = tile * TB + 2 * w;
-    dct4_compress_pair<FK>(v, rk, cx, b0, b0 + bs, true, maxima, indices, list, count, dc);
+    dct4_pair_core<FK, 0>(v, ra, cx, b0 + bs, true, maxima, list, count);
+    // pair 1's rows (read late: registers), then the stage is free
+#pragma unroll
+    for (int a0 = 0; a0 < 4; ++a0) r1[a0] = tma::lds128f(src + rd1 + a0 * 16 * 128);
+    __syncwarp();  // every lane's reads done; exchange area reused by pair 1
+    if (lane == 0) tma::mbar_arrive(ebar0 + 8 * s);  // stage free for the producer
+#pragma unroll
+    for (int a0 = 0; a0 < 4; ++a0) {
+      v[a0 * 4 + 0] = (double)r1[a0].x;
+      v[a0 * 4 + 1] = (double)r1[a0].y;
+      v[a0 * 4 + 2] = (double)r1[a0].z;
+      v[a0 * 4 + 3] = (double)r1[a0].w;
+    }
+    dct4_pair_core<FK, PAIRB>(v, ra, cx, b0 + 2 + bs, true, maxima, list, count);
+    __syncwarp();
+    // ---- the 4 blocks' kept indices: one contiguous run of 4K bytes
+    dct4_copy_out(stg, 2 * K, PAIRB - 2 * K, 4 * K, indices + b0 * (int64_t)K, lane);
+    if (dc && lane < 4) dc[b0 + lane] = stg[(lane >> 1) * PAIRB + (lane & 1) * K];
     __syncwarp();  // staging and exchange area reused by the next tile
   }
 }
