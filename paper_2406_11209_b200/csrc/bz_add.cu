@@ -98,30 +98,6 @@ __device__ __forceinline__ void unpack_chunk(const uint4& w, elem_t<IT> (&out)[1
   }
 }
 
-// deterministic sum of every thread's red_acc into red_ws[1]: warp tree, CTA
-// tree, the last CTA sums the CTA partials in index order (red_ws layout:
-// [arrival counter, result, CTA partials]; the counter is re-armed)
-__device__ __forceinline__ void red_finish(double red_acc, double* __restrict__ red_ws) {
-  for (int o = 16; o > 0; o >>= 1) red_acc += __shfl_xor_sync(0xffffffffu, red_acc, o);
-  __shared__ double wsum[8];
-  __shared__ bool last;
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = red_acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += wsum[i];
-    red_ws[2 + blockIdx.x] = s;
-    last = ticket_arrive(reinterpret_cast<unsigned int*>(red_ws)) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(red_ws + 2 + i);
-    red_ws[1] = s;
-    *reinterpret_cast<unsigned int*>(red_ws) = 0u;  // re-arm
-  }
-}
-
 // mode 0: a + (+/-)b     mode 1: a + shift at the first coefficient (add_scalar)
 // A group of GS lanes handles one block; each lane keeps NCH chunks of V
 // coefficients in registers (GS*NCH*V >= kept), so the block is read once.
@@ -642,6 +618,10 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
       !getenv("BZC_B200_NO_ADD8"))
     return launch_add8(ga, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s,
                        out_dc);
+  // int8 / float32 small unaligned blocks (the C5 low-pass mask): bz_add_small.cu
+  if (sizeof(IT) == 1 && add_small_supported(ga, gb, mode))
+    return launch_add_small(ga, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max,
+                            out_idx, out_dc, s);
   constexpr int V = 16 / sizeof(IT);
   const int kept = ga.kept;
   const int vecs = (kept + V - 1) / V;  // chunks per block
@@ -849,6 +829,8 @@ int launch_subtract_l2(const Geo& ga, const Geo& gb, const void* a_max, const vo
   if (ws_bytes < subtract_l2_workspace()) { set_error("subtract_l2: workspace too small"); return BZ_E_WORKSPACE; }
   if (ga.nblocks == 0 || ga.kept == 0) return cudaMemsetAsync(out, 0, sizeof(double), s) == cudaSuccess ? BZ_OK : BZ_E_CUDA;
   double* w = reinterpret_cast<double*>(ws);
+  if (add_small_supported(ga, gb, 0))  // int8 / float32 small unaligned blocks: bz_add_small.cu
+    return launch_subtract_l2_small(ga, a_max, a_idx, b_max, b_idx, w, out, s);
   int rc = BZ_E_UNSUPPORTED;
   if (ga.index_kind == BZ_I8) rc = launch_subtract_l2_t<int8_t>(ga, gb, a_max, a_idx, b_max, b_idx, w, out, s);
   else if (ga.index_kind == BZ_I16) rc = launch_subtract_l2_t<int16_t>(ga, gb, a_max, a_idx, b_max, b_idx, w, out, s);
@@ -863,8 +845,9 @@ int launch_add(const Geo& ga, const Geo& gb, const void* a_max, const void* a_id
   if (!ga.keeps_first) out_dc = nullptr;
   // the int8 / float32 kernel writes the DC plane itself; the others are
   // followed by a gather of the first coefficients
-  const bool own = ga.index_kind == BZ_I8 && add8_supported(ga, gb, mode, a_idx, b_idx, out_idx) &&
-                   !getenv("BZC_B200_NO_ADD8");
+  const bool own = ga.index_kind == BZ_I8 &&
+                   ((add8_supported(ga, gb, mode, a_idx, b_idx, out_idx) && !getenv("BZC_B200_NO_ADD8")) ||
+                    add_small_supported(ga, gb, mode));
   void* dc_in = own ? out_dc : nullptr;
   int rc;
   switch (ga.index_kind) {

@@ -15,8 +15,8 @@
 // and a midpoint would need j/127 = 1/2).  So x equals the reference's
 // fl(fl(F N) / r) bit for bit.  Subtract negates t_hi and t_lo (exact).
 //
-// Rebinning uses the 24-bit fixed point of bz_dct8.cu (one FMA per
-// coefficient); a block whose maxima are tiny / huge / zero / non-finite,
+// Rebinning uses the 32-bit fixed point of bz_common.cuh (kMagicH: one FMA
+// per coefficient); a block whose maxima are tiny / huge / zero / non-finite,
 // whose stored maximum could round differently, or with a coefficient
 // within one fixed-point unit of a rounding half, is recomputed by the
 // group with the exact IEEE path (codec.py:253-278) right away.
@@ -158,8 +158,8 @@ k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
     }
     const double n = round_to_kind<BZ_F32>(m);
     const BinCtx bc = bin_ctx<false>(n, r, m);
-    // 24-bit fixed point (bz_dct8.cu): index = top byte of y unless the
-    // fraction is within one unit of one half
+    // 32-bit fixed point (kMagicH, bz_common.cuh): index = low byte of the
+    // high word unless the fraction (low word) is within 2^-24 of one half
     unsigned z4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
     uint4 ov[NCH];
 #pragma unroll
@@ -167,18 +167,18 @@ k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
       unsigned y[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const int fx = __double2loint(__fma_rn(c[ch * 16 + e], bc.R, 1.5 * 268435456.0));
-        y[e] = (unsigned)fx + (1u << 23) + 1u;
-        z4[e & 3] = min(z4[e & 3], y[e] & 0xffffffu);
+        const double d = __fma_rn(c[ch * 16 + e], bc.R, kMagicH);
+        y[e] = (unsigned)__double2hiint(d);
+        z4[e & 3] = min(z4[e & 3], (unsigned)__double2loint(d));
       }
       unsigned wd[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        wd[k] = __byte_perm(__byte_perm(y[4 * k], y[4 * k + 1], 0x0073),
-                            __byte_perm(y[4 * k + 2], y[4 * k + 3], 0x0073), 0x5410);
+        wd[k] = __byte_perm(__byte_perm(y[4 * k], y[4 * k + 1], 0x0040),
+                            __byte_perm(y[4 * k + 2], y[4 * k + 3], 0x0040), 0x5410);
       ov[ch] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     }
-    const bool near = min(min(z4[0], z4[1]), min(z4[2], z4[3])) <= 2u;
+    const bool near = min(min(z4[0], z4[1]), min(z4[2], z4[3])) < kNearHalf;
     const bool bad = !safe || !bc.fast || !(m < 1.7976931348623157e308);
     const bool any_bad = (__ballot_sync(gmask, near || bad) & gmask) != 0u;
     if (!any_bad) {

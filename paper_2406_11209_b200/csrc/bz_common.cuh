@@ -43,6 +43,19 @@ __device__ __forceinline__ void record_complete(double* record) {
   *reinterpret_cast<volatile double*>(record + BZ_RECORD_DOUBLES - 1) = 1.0;
 }
 
+// Fixed-point binning of the factored kernels.  With v = c * r / N and
+// |v| < r + 1/2, d = fma(c, r / N, kMagicH) lies in [2^20, 2^21), where one
+// unit of the last place is 2^-32, so d's significand holds
+// 2^19 + v + 1/2 + 2^-24 rounded once to 32 fraction bits:
+//   * high word, low byte: floor(v + 1/2 + 2^-24) mod 256 -- the int8 index
+//     rint(v) (two's complement) unless v is within 2^-24 of a rounding half;
+//   * low word: the 32-bit fraction of v + 1/2 + 2^-24; it is below
+//     kNearHalf = 2^9 exactly when v lies within [-2^-24, 2^-24) of a half
+//     (plus the 2^-33 rounding) -- such a block goes to the exact path.
+// The constant needs 45 significant bits: exact.  (codec.py:272-277)
+constexpr double kMagicH = 1.5 * 1048576.0 + 0.5 + 0x1p-24;
+constexpr unsigned kNearHalf = 512u;
+
 // ------------------------------------------------------------- kind traits --
 template <int K> struct FloatKind;
 template <> struct FloatKind<BZ_BF16> { using T = uint16_t; static constexpr int SIG = 7,  EMIN = -126,  EMAX = 127; };

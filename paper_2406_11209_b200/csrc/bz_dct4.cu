@@ -111,11 +111,8 @@ __device__ __forceinline__ void sts_u8(uint32_t addr, unsigned v) {
   asm volatile("st.shared.u8 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
 }
 
-// 1.5 * 2^28 + 1/2 + 2^-24 (exact: 53 significant bits): fma(c, r/N, kMagicY)
-// leaves y = RN(v * 2^24) + 2^23 + 1 in the low word, v = c r / N -- the
-// index is y's top byte unless the 24-bit fraction y & 0xffffff is <= 2
-// (within one unit of a rounding half; bz_dct8.cu)
-constexpr double kMagicY = 1.5 * 268435456.0 + 0.5 + 0x1p-24;
+// binning constant kMagicH (bz_common.cuh): the index is the low byte of
+// the high word, the low word the near-half test
 
 template <int FK, int OFF>
 __device__ __forceinline__ void dct4_pair_core(double (&v)[16], const uint32_t (&ra)[16],
@@ -169,17 +166,17 @@ __device__ __forceinline__ void dct4_pair_core(double (&v)[16], const uint32_t (
   bool bad = !bc.fast || !(mx < 1.7976931348623157e308) ||
              round_to_kind<FK>(mx * (1.0 - kDeltaRel)) != round_to_kind<FK>(mx * (1.0 + kDeltaRel));
 
-  // ---- bin into the staging bytes (24-bit fixed point, bz_dct8.cu).  The
+  // ---- bin into the staging bytes (32-bit fixed point, kMagicH).  The
   // near-half test runs over all 16 coefficients: a dropped one can only
   // send its block to the exact fix-up needlessly (probability ~2^-22)
   unsigned z4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
-    const unsigned y1 = (unsigned)__double2loint(__fma_rn(v[q], R16, kMagicY));
-    z4[q & 3] = min(z4[q & 3], y1 & 0xffffffu);
-    sts_u8(ra[q] + OFF, y1 >> 24);
+    const double d = __fma_rn(v[q], R16, kMagicH);
+    z4[q & 3] = min(z4[q & 3], (unsigned)__double2loint(d));
+    sts_u8(ra[q] + OFF, (unsigned)__double2hiint(d));  // st.shared.u8 keeps the low byte
   }
-  bad = bad || min(min(z4[0], z4[1]), min(z4[2], z4[3])) <= 2u;
+  bad = bad || min(min(z4[0], z4[1]), min(z4[2], z4[3])) < kNearHalf;
   const unsigned badmask = __ballot_sync(0xffffffffu, bad && valid);
   if (valid && o == 0) {
     store_kind<FK>(maxima, b, n);

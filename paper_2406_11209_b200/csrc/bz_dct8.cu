@@ -296,25 +296,24 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
     bool bad = !bc.fast || !(mx < 1.7976931348623157e308) ||
                round_to_kind<FK>(mx * (1.0 - kDeltaRel)) != round_to_kind<FK>(mx * (1.0 + kDeltaRel));
 
-    // ---- bin: 24-bit fixed point, t = C' * (r / N) rounded once by an FMA
-    // against 1.5 * 2^28 (FastBin<int8_t>); y1 = fx + 2^23 + 1: the index is
-    // the top byte of y1 unless the fraction is within one unit of one half,
-    // i.e. (y1 & 0xffffff) <= 2 -- then the block is flagged (and the byte
-    // may be off by one; the fix-up rewrites it)
+    // ---- bin: 32-bit fixed point (kMagicH, bz_common.cuh): the index is the
+    // low byte of the high word unless the low word (the fraction) is within
+    // 2^-24 of a rounding half -- then the block is flagged (and the byte may
+    // be off by one; the fix-up rewrites it)
     unsigned z4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
     unsigned y[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
-      const int fx = __double2loint(__fma_rn(c[e], bc.R, 1.5 * 268435456.0));
-      y[e] = (unsigned)fx + (1u << 23) + 1u;
-      z4[e & 3] = min(z4[e & 3], y[e] & 0xffffffu);
+      const double d = __fma_rn(c[e], bc.R, kMagicH);
+      y[e] = (unsigned)__double2hiint(d);
+      z4[e & 3] = min(z4[e & 3], (unsigned)__double2loint(d));
     }
-    bad = bad || min(min(z4[0], z4[1]), min(z4[2], z4[3])) <= 2u;
+    bad = bad || min(min(z4[0], z4[1]), min(z4[2], z4[3])) < kNearHalf;
     const unsigned badmask = __ballot_sync(0xffffffffu, bad && valid);
     if (valid) {
       if (o == 0) {
         store_kind<FK>(maxima, b, n);
-        if (dc) dc[b] = (int8_t)(y[0] >> 24);  // DC plane: canonical position 0
+        if (dc) dc[b] = (int8_t)y[0];  // DC plane: canonical position 0
       }
       int8_t* dst = indices + b * (int64_t)BS + hi * 64 + h * 32;
       uint4 wv[2];
@@ -324,7 +323,7 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const unsigned* yy = y + hh * 16 + k * 4;
-          wd[k] = __byte_perm(__byte_perm(yy[0], yy[1], 0x0073), __byte_perm(yy[2], yy[3], 0x0073), 0x5410);
+          wd[k] = __byte_perm(__byte_perm(yy[0], yy[1], 0x0040), __byte_perm(yy[2], yy[3], 0x0040), 0x5410);
         }
         wv[hh] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
       }

@@ -401,4 +401,30 @@ __device__ __forceinline__ void smem_to_tile(unsigned char* g, const unsigned ch
   for (int64_t i = h + body * 16 + t; i < nbytes; i += nt) g[i] = st[mis + i];
 }
 
+// deterministic sum of every thread's red_acc into red_ws[1]: warp tree, CTA
+// tree, the last CTA sums the CTA partials in index order (red_ws layout:
+// [arrival counter, result, CTA partials]; the counter is re-armed)
+__device__ __forceinline__ void red_finish(double red_acc, double* __restrict__ red_ws,
+                                           double* __restrict__ out = nullptr) {
+  for (int o = 16; o > 0; o >>= 1) red_acc += __shfl_xor_sync(0xffffffffu, red_acc, o);
+  __shared__ double wsum[8];
+  __shared__ bool last;
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = red_acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += wsum[i];
+    red_ws[2 + blockIdx.x] = s;
+    last = ticket_arrive(reinterpret_cast<unsigned int*>(red_ws)) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(red_ws + 2 + i);
+    red_ws[1] = s;
+    if (out) *out = s;
+    *reinterpret_cast<unsigned int*>(red_ws) = 0u;  // re-arm
+  }
+}
+
 }  // namespace bz

@@ -452,3 +452,42 @@ def test_negative_dominant_coefficients(bz, shape, block, mask):
                       (bz.subtract(cb, ca), o.subtract(rb, ra))):
         assert np.array_equal(got.maxima_f64().cpu().numpy(), want.maxima)
         assert np.array_equal(got.indices.cpu().numpy(), want.indices)
+
+
+@pytest.mark.parametrize("keep", [1, 3, 9, 15, 17, 31, 47, 66, 95, 127])
+def test_add_small_kernel_every_group_width(bz, keep):
+    """bz_add_small.cu (int8 / float32 blocks, kept count not a multiple of
+    16, one template per ceil(K / 8)): add / subtract / add_scalar /
+    subtract+l2 bit-exact with the oracle for K across every lane width,
+    over a grid of several tiles with zero, tiny, huge and NaN blocks and
+    exact-path (near-half) blocks from nearly equal operands."""
+    block = (4, 4, 8)
+    rng = np.random.default_rng(1000 + keep)
+    grid = (9, 7, 5)  # 315 blocks: several tiles for every K
+    shape = tuple(b * g for b, g in zip(block, grid))
+    bits = np.zeros(128, bool)
+    bits[0] = True
+    bits[1 + rng.permutation(127)[:keep - 1]] = True
+    bits = bits.reshape(block)
+    s = _settings(bz, block, "f32", "i8", mask_bits=bits)
+    os_ = o.Settings(block, "f32", "i8", "dct", bits)
+    xa = rng.normal(size=shape)
+    xb = xa + 1e-3 * rng.normal(size=shape)  # near-cancelling: small coefficients
+    xa[:4, :4, :8] = 0.0
+    xb[4:8, :4, :8] = np.nan
+    xa[8:12, :4, :8] *= 1e-38
+    xb[12:16, :4, :8] *= 1e37
+    ra, rb = o.compress(o.round_to_kind(xa, "f32"), os_), o.compress(o.round_to_kind(xb, "f32"), os_)
+    a = bz.CompressedArray(shape, s, ra.maxima, ra.indices)
+    b = bz.CompressedArray(shape, s, rb.maxima, rb.indices)
+    for got, want in ((bz.add(a, b), o.add(ra, rb)), (bz.subtract(a, b), o.subtract(ra, rb)),
+                      (bz.add_scalar(a, -0.75), o.add_scalar(ra, -0.75))):
+        assert np.array_equal(got.maxima_f64().cpu().numpy(), want.maxima, equal_nan=True)
+        assert np.array_equal(got.indices.cpu().numpy(), want.indices)
+        assert torch.equal(got.dc_plane, got.indices[..., 0])
+    assert math.isnan(bz.subtract_l2(a, b))
+    xb[4:8, :4, :8] = 0.5
+    rb = o.compress(o.round_to_kind(xb, "f32"), os_)
+    b = bz.CompressedArray(shape, s, rb.maxima, rb.indices)
+    got, want = bz.subtract_l2(b, a), o.l2_norm(o.subtract(rb, ra))
+    assert math.isclose(got, want, rel_tol=1e-12), (got, want)
