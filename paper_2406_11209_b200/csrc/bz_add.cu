@@ -619,7 +619,7 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
     return launch_add8(ga, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s,
                        out_dc);
   // int8 / float32 small unaligned blocks (the C5 low-pass mask): bz_add_small.cu
-  if (sizeof(IT) == 1 && add_small_supported(ga, gb, mode))
+  if (sizeof(IT) == 1 && add_small_supported(ga, gb, mode, a_max, a_idx, b_max, b_idx, out_idx))
     return launch_add_small(ga, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max,
                             out_idx, out_dc, s);
   constexpr int V = 16 / sizeof(IT);
@@ -829,8 +829,10 @@ int launch_subtract_l2(const Geo& ga, const Geo& gb, const void* a_max, const vo
   if (ws_bytes < subtract_l2_workspace()) { set_error("subtract_l2: workspace too small"); return BZ_E_WORKSPACE; }
   if (ga.nblocks == 0 || ga.kept == 0) return cudaMemsetAsync(out, 0, sizeof(double), s) == cudaSuccess ? BZ_OK : BZ_E_CUDA;
   double* w = reinterpret_cast<double*>(ws);
-  if (add_small_supported(ga, gb, 0))  // int8 / float32 small unaligned blocks: bz_add_small.cu
+  if (add_small_supported(ga, gb, 0, a_max, a_idx, b_max, b_idx, nullptr))  // bz_add_small.cu
     return launch_subtract_l2_small(ga, a_max, a_idx, b_max, b_idx, w, out, s);
+  if (add8_supported(ga, gb, 0, a_idx, b_idx, a_idx) && !getenv("BZC_B200_NO_ADD8"))  // bz_add8.cu
+    return launch_subtract_l2_add8(ga, a_max, a_idx, b_max, b_idx, w, out, s);
   int rc = BZ_E_UNSUPPORTED;
   if (ga.index_kind == BZ_I8) rc = launch_subtract_l2_t<int8_t>(ga, gb, a_max, a_idx, b_max, b_idx, w, out, s);
   else if (ga.index_kind == BZ_I16) rc = launch_subtract_l2_t<int16_t>(ga, gb, a_max, a_idx, b_max, b_idx, w, out, s);
@@ -847,7 +849,7 @@ int launch_add(const Geo& ga, const Geo& gb, const void* a_max, const void* a_id
   // followed by a gather of the first coefficients
   const bool own = ga.index_kind == BZ_I8 &&
                    ((add8_supported(ga, gb, mode, a_idx, b_idx, out_idx) && !getenv("BZC_B200_NO_ADD8")) ||
-                    add_small_supported(ga, gb, mode));
+                    add_small_supported(ga, gb, mode, a_max, a_idx, b_max, b_idx, out_idx));
   void* dc_in = own ? out_dc : nullptr;
   int rc;
   switch (ga.index_kind) {

@@ -30,8 +30,8 @@ namespace {
 
 // exact per-block path (rare): IEEE product, division, NaN-propagating
 // maximum and exact binning, GS lanes of the group cooperating
-template <int GS, int MODE>
-__device__ __noinline__ void add8_block_exact(int64_t b, int kept, int sub, unsigned gmask,
+template <int GS, int MODE, bool RED = false>
+__device__ __noinline__ double add8_block_exact(int64_t b, int kept, int sub, unsigned gmask,
                                               const float* __restrict__ a_max,
                                               const int8_t* __restrict__ a_idx,
                                               const float* __restrict__ b_max,
@@ -59,21 +59,35 @@ __device__ __noinline__ void add8_block_exact(int64_t b, int kept, int sub, unsi
     m = (isnan(t) || isnan(m)) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(m, t);
   }
   const double n = round_to_kind<BZ_F32>(m);
+  if (RED) {  // fused l2 of the rebinned difference: this lane's sum of squares
+    int sq = 0;
+    for (int k = sub; k < kept; k += GS) {
+      const int q = (int)bin_exact(coeff(k), n, r, r);
+      sq += q * q;
+    }
+    return __fma_rn((double)sq * n, n, 0.0);
+  }
   if (sub == 0) out_max[b] = (float)n;
   for (int k = sub; k < kept; k += GS) out_idx[base + k] = (int8_t)bin_exact(coeff(k), n, r, r);
   if (out_dc && sub == 0) out_dc[b] = (int8_t)bin_exact(coeff(0), n, r, r);
+  return 0.0;
 }
 
 }  // namespace
 
 // GS lanes per block, NCH 16-byte chunks (16 indices) per lane; the next
 // block's chunks and maxima are loaded while the current block computes.
-template <int GS, int NCH, int MODE>
+// RED: the fused l2_norm(subtract(a, b)) of the time-series workflow
+// (cli.py:240-243) -- the rebinned indices are squared and summed (dp4a)
+// times N^2 instead of stored; the last CTA writes the sum to red_out.
+template <int GS, int NCH, int MODE, bool RED = false>
 __global__ void __launch_bounds__(256, NCH == 1 ? 3 : 2)
 k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
        const int8_t* __restrict__ a_idx, const float* __restrict__ b_max,
        const int8_t* __restrict__ b_idx, int subtract, double shift,
-       float* __restrict__ out_max, int8_t* __restrict__ out_idx, int8_t* __restrict__ out_dc) {
+       float* __restrict__ out_max, int8_t* __restrict__ out_idx, int8_t* __restrict__ out_dc,
+       double* __restrict__ red_ws = nullptr, double* __restrict__ red_out = nullptr) {
+  double red_acc = 0.0;
   constexpr double r = 127.0, rinv = 1.0 / 127.0;
   constexpr int L = NCH * 16;
   const int lane = threadIdx.x & 31;
@@ -182,20 +196,36 @@ k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
     const bool bad = !safe || !bc.fast || !(m < 1.7976931348623157e308);
     const bool any_bad = (__ballot_sync(gmask, near || bad) & gmask) != 0u;
     if (!any_bad) {
-      if (sub == 0) {
-        out_max[b] = (float)n;
-        if (out_dc) out_dc[b] = (int8_t)ov[0].x;  // DC plane: flat position 0
-      }
+      if constexpr (RED) {
+        int sq = 0;  // <= 32 * 127^2 per chunk: exact in int32
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        const int k0 = (ch * GS + sub) * 16;
-        if (k0 < kept) __stcs(reinterpret_cast<uint4*>(out_idx + base + k0), ov[ch]);
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int k0 = (ch * GS + sub) * 16;
+          if (k0 < kept) {
+            sq = __dp4a((int)ov[ch].x, (int)ov[ch].x, sq);
+            sq = __dp4a((int)ov[ch].y, (int)ov[ch].y, sq);
+            sq = __dp4a((int)ov[ch].z, (int)ov[ch].z, sq);
+            sq = __dp4a((int)ov[ch].w, (int)ov[ch].w, sq);
+          }
+        }
+        red_acc = __fma_rn((double)sq * n, n, red_acc);  // (i N) N: overflow-safe
+      } else {
+        if (sub == 0) {
+          out_max[b] = (float)n;
+          if (out_dc) out_dc[b] = (int8_t)ov[0].x;  // DC plane: flat position 0
+        }
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int k0 = (ch * GS + sub) * 16;
+          if (k0 < kept) __stcs(reinterpret_cast<uint4*>(out_idx + base + k0), ov[ch]);
+        }
       }
     } else {  // group-uniform: the exact path for this block
-      add8_block_exact<GS, MODE>(b, kept, sub, gmask, a_max, a_idx, b_max, b_idx, subtract, shift,
-                                 out_max, out_idx, out_dc);
+      red_acc += add8_block_exact<GS, MODE, RED>(b, kept, sub, gmask, a_max, a_idx, b_max, b_idx,
+                                                 subtract, shift, out_max, out_idx, out_dc);
     }
   }
+  if constexpr (RED) red_finish(red_acc, red_ws, red_out);
 }
 
 bool add8_supported(const Geo& ga, const Geo& gb, int mode, const void* a_idx, const void* b_idx,
@@ -232,6 +262,31 @@ int launch_add8(const Geo& ga, const void* a_max, const void* a_idx, const void*
 #undef BZ_A8M
 #undef BZ_A8
   return check_launch("add8");
+}
+
+// l2_norm(subtract(a, b))^2 into red_ws[1] and *out (the subtract_l2
+// workspace contract: at most 3 * kSMs CTAs)
+int launch_subtract_l2_add8(const Geo& ga, const void* a_max, const void* a_idx,
+                            const void* b_max, const void* b_idx, double* red_ws, double* out,
+                            cudaStream_t s) {
+  const int vecs = ga.kept / 16;
+  int GS = 1;
+  while (GS < 32 && GS < vecs) GS <<= 1;
+  const int NCH = (vecs + GS - 1) / GS;  // 1 or 2
+  const int grid = grid_for(ga.nblocks * GS, 256, 3);
+#define BZ_R8(G, N)                                                                           \
+  k_add8<G, N, 0, true><<<grid, 256, 0, s>>>(ga.nblocks, ga.kept, (const float*)a_max,        \
+                                             (const int8_t*)a_idx, (const float*)b_max,       \
+                                             (const int8_t*)b_idx, 1, 0.0, nullptr, nullptr,  \
+                                             nullptr, red_ws, out)
+#define BZ_R8G(G)                                   \
+  case G:                                           \
+    if (NCH == 1) BZ_R8(G, 1); else BZ_R8(G, 2);    \
+    break;
+  switch (GS) { BZ_R8G(1) BZ_R8G(2) BZ_R8G(4) BZ_R8G(8) BZ_R8G(16) BZ_R8G(32) }
+#undef BZ_R8G
+#undef BZ_R8
+  return check_launch("subtract_l2_add8");
 }
 
 }  // namespace bz

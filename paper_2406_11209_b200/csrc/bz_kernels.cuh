@@ -96,13 +96,18 @@ int launch_add8(const Geo& ga, const void* a_max, const void* a_idx, const void*
                 void* out_idx, cudaStream_t s, void* out_dc = nullptr);
 // int8 / float32 blocks whose kept indices are not whole 16-byte vectors
 // (K <= 128; bz_add_small.cu)
-bool add_small_supported(const Geo& ga, const Geo& gb, int mode);
+bool add_small_supported(const Geo& ga, const Geo& gb, int mode, const void* a_max,
+                         const void* a_idx, const void* b_max, const void* b_idx,
+                         const void* out_idx);
 int launch_add_small(const Geo& ga, const void* a_max, const void* a_idx, const void* b_max,
                      const void* b_idx, int subtract, double shift, int mode, void* out_max,
                      void* out_idx, void* out_dc, cudaStream_t s);
 int launch_subtract_l2_small(const Geo& ga, const void* a_max, const void* a_idx,
                              const void* b_max, const void* b_idx, double* red_ws, double* out,
                              cudaStream_t s);
+int launch_subtract_l2_add8(const Geo& ga, const void* a_max, const void* a_idx,
+                            const void* b_max, const void* b_idx, double* red_ws, double* out,
+                            cudaStream_t s);
 int launch_add(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                const void* b_max, const void* b_idx, int subtract, double shift, int mode,
                void* out_max, void* out_idx, cudaStream_t s, void* out_dc = nullptr);
