@@ -131,7 +131,7 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
       const void* __restrict__ a_max, const IT* __restrict__ a_idx,
       const void* __restrict__ b_max, const IT* __restrict__ b_idx, int subtract,
       double shift, int mode_rt, void* __restrict__ out_max, IT* __restrict__ out_idx,
-      double* __restrict__ red_ws = nullptr) {
+      double* __restrict__ red_ws = nullptr, IT* __restrict__ out_dc = nullptr) {
   double red_acc = 0.0;
   constexpr int mode = MODE;
   (void)mode_rt;
@@ -273,6 +273,10 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
           else q64[e] = 0;
           if (nr || !bc.fast || sizeof(IT) == 8) q64[e] = bin_exact_ctx(c[ch * V + e], bc, r, bound);
         }
+      }
+      if (!RED && out_dc && k0 == 0) {  // DC plane: flat position 0
+        if constexpr (sizeof(IT) <= 2) out_dc[b] = (IT)q[0];
+        else out_dc[b] = (IT)q64[0];
       }
       if constexpr (RED) {
         if constexpr (sizeof(IT) <= 2) {
@@ -612,7 +616,9 @@ k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
 template <typename IT>
 static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                         const void* b_max, const void* b_idx, int subtract, double shift,
-                        int mode, void* out_max, void* out_idx, cudaStream_t s, void* out_dc) {
+                        int mode, void* out_max, void* out_idx, cudaStream_t s, void* out_dc,
+                        bool& dc_done) {
+  dc_done = true;  // every path below writes the DC plane itself, except the tiled / staged ones
   // int8 indices with float32 maxima, whole 16-byte chunks: bz_add8.cu
   if (sizeof(IT) == 1 && add8_supported(ga, gb, mode, a_idx, b_idx, out_idx) &&
       !getenv("BZC_B200_NO_ADD8"))
@@ -633,6 +639,7 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
     while (GS < 32 && GS < vecs) GS <<= 1;
     NCH = (vecs + GS - 1) / GS;
     if (NCH > 4) {  // too large to hold in registers: the general warp-per-block kernel
+      dc_done = false;
       const int g = grid_for(ga.nblocks * 32, 256, 4);
       if (mode == 0)
         k_add_general<IT, 0><<<g, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind, gb.float_kind,
@@ -655,6 +662,7 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
   const bool same_fk = ga.float_kind == gb.float_kind || mode != 0;
   // unaligned blocks of I8 / I16 indices: shared-memory staged tiles
   if constexpr (sizeof(IT) <= 2) {
+    dc_done = false;
     const int64_t bpb = (int64_t)kept * sizeof(IT);
     if ((bpb % 16) != 0 && kept >= 8 && bpb <= 2048 && same_fk &&
         (ga.float_kind == BZ_F32 || ga.float_kind == BZ_F64)) {
@@ -706,12 +714,13 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
       else { if (mode == 0) BZ_ST(BZ_F32, 0) else BZ_ST(BZ_F32, 1) }
 #undef BZ_ST
     }
+    dc_done = true;
   }
 #define BZ_K(G, N, V, F, M)                                                                    \
   k_add<IT, G, N, V, F, M><<<grid, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind, gb.float_kind, \
                                                ga.float_kind, a_max, (const IT*)a_idx, b_max,  \
                                                (const IT*)b_idx, subtract, shift, mode,        \
-                                               out_max, (IT*)out_idx)
+                                               out_max, (IT*)out_idx, nullptr, (IT*)out_dc)
 #define BZ_LAUNCH(G, N)                                                              \
   do {                                                                               \
     if (vec && same_fk && ga.float_kind == BZ_F64) {                                 \
@@ -845,18 +854,15 @@ int launch_add(const Geo& ga, const Geo& gb, const void* a_max, const void* a_id
                void* out_max, void* out_idx, cudaStream_t s, void* out_dc) {
   if (ga.nblocks == 0) return BZ_OK;
   if (!ga.keeps_first) out_dc = nullptr;
-  // the int8 / float32 kernel writes the DC plane itself; the others are
-  // followed by a gather of the first coefficients
-  const bool own = ga.index_kind == BZ_I8 &&
-                   ((add8_supported(ga, gb, mode, a_idx, b_idx, out_idx) && !getenv("BZC_B200_NO_ADD8")) ||
-                    add_small_supported(ga, gb, mode, a_max, a_idx, b_max, b_idx, out_idx));
-  void* dc_in = own ? out_dc : nullptr;
+  // the kernels write the DC plane themselves; the tiled / staged ones and the
+  // warp-per-block general kernel are followed by a gather of first coefficients
+  bool own = false;
   int rc;
   switch (ga.index_kind) {
-    case BZ_I8: rc = launch_add_t<int8_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, dc_in); break;
-    case BZ_I16: rc = launch_add_t<int16_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, dc_in); break;
-    case BZ_I32: rc = launch_add_t<int32_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, dc_in); break;
-    default: rc = launch_add_t<int64_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, dc_in); break;
+    case BZ_I8: rc = launch_add_t<int8_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, out_dc, own); break;
+    case BZ_I16: rc = launch_add_t<int16_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, out_dc, own); break;
+    case BZ_I32: rc = launch_add_t<int32_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, out_dc, own); break;
+    default: rc = launch_add_t<int64_t>(ga, gb, a_max, a_idx, b_max, b_idx, subtract, shift, mode, out_max, out_idx, s, out_dc, own); break;
   }
   if (rc || !out_dc || own) return rc;
   return launch_extract_dc(ga, out_idx, out_dc, s);

@@ -182,7 +182,7 @@ static int compress_body(const bz_layout* L, const Geo& g, const void* x, int x_
     size_t need = (size_t)dense_count(L) * float_kind_bytes(L->float_kind);
     if (!ws || ws_bytes < need) { set_error("compress: workspace too small for conversion"); return BZ_E_WORKSPACE; }
     if (int rc = launch_round_to_kind(x, x_kind, ws, L->float_kind, dense_count(L), nullptr, s)) return rc;
-    return launch_fast_compress(g, ws, maxima, indices, s);
+    return launch_fast_compress(g, ws, maxima, indices, s, dc, &dc_done);
   }
   if (!force_generic() && dct8_compress_supported(g, x_kind) && ws &&
       ws_bytes >= dct8_compress_workspace(g)) {
@@ -195,7 +195,7 @@ static int compress_body(const bz_layout* L, const Geo& g, const void* x, int x_
     return launch_dct4_compress(g, x, maxima, indices, ws, ws_bytes, s, dc);
   }
   if (!force_generic() && fast_supported(g, x_kind))
-    return launch_fast_compress(g, x, maxima, indices, s);
+    return launch_fast_compress(g, x, maxima, indices, s, dc, &dc_done);
   dc_done = true;
   return launch_exact_compress(g, x, x_kind, maxima, indices, nullptr, nullptr, g.nblocks, ws,
                                ws_bytes, s, dc);

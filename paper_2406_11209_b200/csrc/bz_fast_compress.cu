@@ -46,7 +46,7 @@ __device__ __forceinline__ uint32_t idx_bits(int q) {
 template <int D, int E, typename TIn, int FK, typename IT, bool PREFETCH = false>
 __global__ void __launch_bounds__(Tile<D, E>::NT)
 k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict__ maxima,
-                IT* __restrict__ indices) {
+                IT* __restrict__ indices, IT* __restrict__ dc) {
   using TL = Tile<D, E>;
   constexpr int NIN = TL::NIN, TB = TL::TB, BS = TL::BS, BPC = TL::BPC, NT = TL::NT;
   constexpr int LP = 0, LQ = D - 1;  // loaded slice axes
@@ -232,6 +232,7 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
               for (int e = 0; e < PER; ++e) q[e] = bin_q(v[cch * PER + e]);
             }
             __stcs(reinterpret_cast<uint4*>(dst) + cch, pack16<IT>(q));
+            if (cch == 0 && o == 0 && dc) dc[b] = (IT)q[0];  // DC plane: position 0
           }
         } else if constexpr ((NIN * sizeof(IT)) % 16 == 0) {
           constexpr int PER = 16 / sizeof(IT);
@@ -241,10 +242,15 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
 #pragma unroll
             for (int e = 0; e < PER; ++e) q[e] = bin_q(v[cch * PER + e]);
             __stcs(reinterpret_cast<uint4*>(dst) + cch, pack16<IT>(q));
+            if (cch == 0 && o == 0 && dc) dc[b] = (IT)q[0];
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < NIN; ++q) dst[q] = (IT)bin_q(v[q]);
+          for (int q = 0; q < NIN; ++q) {
+            const IT qv = (IT)bin_q(v[q]);
+            dst[q] = qv;
+            if (q == 0 && o == 0 && dc) dc[b] = qv;
+          }
         }
       }
     } else {
@@ -256,7 +262,11 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
 #pragma unroll
         for (int q = 0; q < NIN; ++q) {
           const int rk = rks[o * NIN + q];
-          if (rk >= 0) st[lb * f.kept + rk] = (IT)bin_q(v[q]);
+          if (rk >= 0) {
+            const IT qv = (IT)bin_q(v[q]);
+            st[lb * f.kept + rk] = qv;
+            if (q == 0 && o == 0 && dc) dc[b] = qv;  // position 0 (dc only when kept)
+          }
         }
       }
       __syncthreads();
@@ -273,7 +283,8 @@ k_fast_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
 
 // ----------------------------------------------------------------- dispatch --
 template <int D, int E, typename TIn, int FK, typename IT>
-static int launch_one(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s) {
+static int launch_one(const Geo& g, const void* x, void* maxima, void* indices, void* dc,
+                      cudaStream_t s) {
   using TL = Tile<D, E>;
   FastParams p;
   if (!make_fast_params(g, TL::BPC, x, sizeof(TIn), p)) {
@@ -292,17 +303,18 @@ static int launch_one(const Geo& g, const void* x, void* maxima, void* indices, 
   int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * occ);
   if (grid < 1) return BZ_OK;
   kern<<<(int)grid, TL::NT, smem, s>>>(p, reinterpret_cast<const TIn*>(x), maxima,
-                                       reinterpret_cast<IT*>(indices));
+                                       reinterpret_cast<IT*>(indices), reinterpret_cast<IT*>(dc));
   return check_launch("fast_compress");
 }
 
 template <int D, int E>
-static int dispatch_kinds(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s) {
-#define BZ_IDX(TIN, FKV)                                                                      \
-  switch (g.index_kind) {                                                                     \
-    case BZ_I8: return launch_one<D, E, TIN, FKV, int8_t>(g, x, maxima, indices, s);   \
-    case BZ_I16: return launch_one<D, E, TIN, FKV, int16_t>(g, x, maxima, indices, s); \
-    case BZ_I32: return launch_one<D, E, TIN, FKV, int32_t>(g, x, maxima, indices, s); \
+static int dispatch_kinds(const Geo& g, const void* x, void* maxima, void* indices, void* dc,
+                          cudaStream_t s) {
+#define BZ_IDX(TIN, FKV)                                                                          \
+  switch (g.index_kind) {                                                                         \
+    case BZ_I8: return launch_one<D, E, TIN, FKV, int8_t>(g, x, maxima, indices, dc, s);   \
+    case BZ_I16: return launch_one<D, E, TIN, FKV, int16_t>(g, x, maxima, indices, dc, s); \
+    case BZ_I32: return launch_one<D, E, TIN, FKV, int32_t>(g, x, maxima, indices, dc, s); \
   }
   if (g.float_kind == BZ_F32) { BZ_IDX(float, BZ_F32) }
   if (g.float_kind == BZ_F64) { BZ_IDX(double, BZ_F64) }
@@ -334,13 +346,16 @@ bool fast_supported(const Geo& g, int x_kind) {
   return false;
 }
 
-int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s) {
+int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s,
+                         void* dc, bool* dc_done) {
   int E;
   uniform_block(g, E);
+  if (dc_done) *dc_done = false;
   if (g.ndim == 3 && E == 8)
     return launch_half3_compress(g, x, maxima, indices, s);
+  if (dc_done) *dc_done = dc != nullptr;
 #define BZ_CASE(DD, EE) \
-  if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, x, maxima, indices, s);
+  if (g.ndim == DD && E == EE) return dispatch_kinds<DD, EE>(g, x, maxima, indices, dc, s);
   BZ_CASE(1, 4) BZ_CASE(1, 8) BZ_CASE(2, 4) BZ_CASE(2, 8) BZ_CASE(3, 4) BZ_CASE(3, 8)
   BZ_CASE(4, 4)
 #undef BZ_CASE

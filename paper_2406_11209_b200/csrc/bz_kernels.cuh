@@ -34,7 +34,10 @@ int launch_exact_decompress(const Geo& g, const void* maxima, const void* indice
 
 // fused fast paths (bz_fast_*.cu)
 bool fast_supported(const Geo& g, int x_kind);
-int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s);
+// dc (optional): the DC plane, written by every path but the 8^3 half-slice
+// one (*dc_done reports which)
+int launch_fast_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s,
+                         void* dc = nullptr, bool* dc_done = nullptr);
 bool fast_decompress_supported(const Geo& g, int out_kind);
 // 8x8x8 blocks, half slices (bz_half3.cu)
 int launch_half3_compress(const Geo& g, const void* x, void* maxima, void* indices, cudaStream_t s);
