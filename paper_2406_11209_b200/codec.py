@@ -12,6 +12,7 @@ in the index kind's dtype -- as CUDA tensors.  ``compress`` and
 from __future__ import annotations
 
 import ctypes
+import math
 import threading
 
 import numpy as np
@@ -236,7 +237,7 @@ class CompressedArray:
     operand's unchanged maxima or indices (negate, mul_scalar).
     """
 
-    __slots__ = ("original_shape", "settings", "maxima", "indices", "_lay", "_dc")
+    __slots__ = ("original_shape", "settings", "maxima", "indices", "_lay", "_dc", "_dev", "_nb")
 
     def __init__(self, original_shape, settings: CodecSettings, maxima, indices, *,
                  _trusted: bool = False, dc=None):
@@ -273,11 +274,19 @@ class CompressedArray:
 
     @property
     def block_count(self) -> int:
-        return int(np.prod(self.block_grid))
+        nb = getattr(self, "_nb", None)  # immutable: computed once
+        if nb is None:
+            nb = math.prod(self.block_grid)
+            object.__setattr__(self, "_nb", nb)
+        return nb
 
     @property
     def device(self) -> torch.device:
-        return self.indices.device
+        dev = getattr(self, "_dev", None)
+        if dev is None:
+            dev = self.indices.device
+            object.__setattr__(self, "_dev", dev)
+        return dev
 
     @property
     def dc_plane(self) -> torch.Tensor | None:

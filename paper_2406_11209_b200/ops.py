@@ -278,8 +278,9 @@ def moments_record(a: CompressedArray, b: CompressedArray | None = None, *,
     Lb = b.layout() if pair else La
     bm = bi = None
     if pair:
-        bm = b.maxima if b.device == dev else b.maxima.to(dev)
-        bi = b.indices if b.device == dev else b.indices.to(dev)
+        same = b.device == dev
+        bm = b.maxima if same else b.maxima.to(dev)
+        bi = b.indices if same else b.indices.to(dev)
         if b.settings.index_kind is not a.settings.index_kind:
             # mixed index kinds are legal for reductions (ops.py:100-116): widen
             wide = max(a.settings.index_kind, b.settings.index_kind, key=lambda k: k.bits)
@@ -382,7 +383,10 @@ def _global_shape(a):
 
 
 def _global_blocks(a) -> int:
-    return int(np.prod(a.settings.grid_for(_global_shape(a))))
+    gs = getattr(a, "global_shape", None)
+    if gs is None:
+        return a.block_count  # cached on the array
+    return math.prod(a.settings.grid_for(gs))
 
 
 def _dot_from(rec: Record, keeps_first: bool) -> float:
@@ -427,7 +431,7 @@ def mean(a: CompressedArray, padding_corrected: bool = False) -> float:
     c = a.settings.block_mean_scale
     firsts_mean = rec.mean_a / _radius(a)
     if padding_corrected:
-        return float(c * (firsts_mean * rec.n) / np.prod(_global_shape(a)))
+        return float(c * (firsts_mean * rec.n) / math.prod(_global_shape(a)))
     return float(firsts_mean / c)
 
 

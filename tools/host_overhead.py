@@ -31,12 +31,29 @@ st = torch.cuda.current_stream()
 h = ops._host_record()
 La = a.layout()
 ws = ops._reduce_workspace(a.device, La)
+b = bz.compress(fill((64, 64, 64), bz.FloatKind.F32, 2), s)
 print(f"mean (public)              {us(lambda: bz.mean(a)):7.2f} us")
+print(f"covariance (public)        {us(lambda: bz.covariance(a, b)):7.2f} us")
+print(f"ssim (public)              {us(lambda: bz.ssim(a, b)):7.2f} us")
+print(f"dot (public)               {us(lambda: bz.dot(a, b)):7.2f} us")
+print(f"_check_compatible          {us(lambda: ops._check_compatible(a, b)):7.2f} us")
 print(f"l2_norm (public)           {us(lambda: bz.l2_norm(a)):7.2f} us")
 print(f"_reduce(dc_only=1)         {us(lambda: ops._reduce(a, dc_only=True)):7.2f} us")
 print(f"moments_record -> pinned   {us(lambda: ops.moments_record(a, dc_only=1, out=h)):7.2f} us")
 print(f"  + stream sync            {us(lambda: (ops.moments_record(a, dc_only=1, out=h), st.synchronize())):7.2f} us")
 print(f"raw ctypes bz_moments_dc   {us(lambda: _native.call('bz_moments_dc', __import__('ctypes').byref(La), a.maxima.data_ptr(), a.dc_plane.data_ptr(), h.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)):7.2f} us")
+lib = _native.load_library()
+tiny = torch.zeros(16, dtype=torch.int8, device="cuda")
+print(f"ctypes bz_version()        {us(lambda: lib.bz_version()):7.2f} us")
+print(f"ctypes bz_negate launch    {us(lambda: lib.bz_negate(0, tiny.data_ptr(), tiny.data_ptr(), 16, st.cuda_stream)):7.2f} us")
+print(f"ctypes bz_moments_dc bad L {us(lambda: lib.bz_moments_dc(None, 0, 0, 0, 0, 0, st.cuda_stream)):7.2f} us")
+print(f"torch tiny kernel launch   {us(lambda: tiny.neg_()):7.2f} us")
+mo = torch.empty_like(a.maxima)
+import ctypes as _ct
+print(f"ctypes bz_mul_scalar       {us(lambda: lib.bz_mul_scalar(_ct.byref(La), a.maxima.data_ptr(), a.indices.data_ptr(), None, 0.5, mo.data_ptr(), None, None, st.cuda_stream)):7.2f} us")
+rec_d = torch.empty(16, dtype=torch.float64, device="cuda")
+print(f"ctypes bz_moments_dc dev   {us(lambda: lib.bz_moments_dc(_ct.byref(La), a.maxima.data_ptr(), a.dc_plane.data_ptr(), rec_d.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)):7.2f} us")
+print(f"ctypes bz_moments sums     {us(lambda: lib.bz_moments(_ct.byref(La), _ct.byref(La), a.maxima.data_ptr(), a.indices.data_ptr(), None, None, 0, 2, rec_d.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)):7.2f} us")
 print(f"a.layout()                 {us(lambda: a.layout()):7.2f} us")
 print(f"_reduce_workspace          {us(lambda: ops._reduce_workspace(a.device, La)):7.2f} us")
 print(f"stream_handle              {us(lambda: _native.stream_handle(a.device)):7.2f} us")
