@@ -135,6 +135,29 @@ __device__ __forceinline__ double load_kind(const void* p, int64_t i) {
     return (double)__uint_as_float(b);
   }
 }
+// Predicated streaming loads that leave 0 when `pred` is false, without a
+// select on the loaded value (a select -- or a register move -- of a pending
+// load result waits for the load, which defeats a prefetch).
+__device__ __forceinline__ uint32_t ld_cs_u32_or0(const void* p, bool pred) {
+  uint32_t v;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b32 %0, 0;\n"
+               " @q ld.global.cs.u32 %0, [%1];\n}\n"
+               : "=r"(v) : "l"(p), "r"((int)pred) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_cs_u64_or0(const void* p, bool pred) {
+  uint64_t v;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b64 %0, 0;\n"
+               " @q ld.global.cs.u64 %0, [%1];\n}\n"
+               : "=l"(v) : "l"(p), "r"((int)pred) : "memory");
+  return v;
+}
+
+// widen one stored value (FloatKind<K>::T) to f64
+template <int K>
+__device__ __forceinline__ double widen_kind(typename FloatKind<K>::T v) {
+  return load_kind<K>(&v, 0);
+}
 __device__ __forceinline__ double load_kind_rt(const void* p, int64_t i, int k) {
   switch (k) {
     case BZ_BF16: return load_kind<BZ_BF16>(p, i);

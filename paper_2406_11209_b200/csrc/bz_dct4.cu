@@ -449,10 +449,15 @@ k_dct4_compress_tma(const __grid_constant__ CUtensorMap xmap, const FastParams p
 }
 
 // ------------------------------------------------------------- decompress --
-template <typename IT, int FK, typename TOut>
-__global__ void __launch_bounds__(256, 3)
+// TST: the warp's two blocks (adjacent along the last axis) leave as one TMA
+// box store (4 x 4 x 4 x 8 elements) from a per-warp, double-buffered
+// shared-memory box instead of per-lane row stores with address arithmetic
+// and bounds checks (the TMA unit clips partial blocks at the array edges).
+template <typename IT, int FK, typename TOut, bool TST = false>
+__global__ void __launch_bounds__(256, TST ? 2 : 3)
 k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
-                  const IT* __restrict__ indices, TOut* __restrict__ out) {
+                  const IT* __restrict__ indices, TOut* __restrict__ out,
+                  const __grid_constant__ CUtensorMap omap) {
   using namespace d4;
   const FastGeo& f = p.f;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -487,37 +492,60 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
   const bool words = ((uintptr_t)indices % 4 == 0) && (tile_bytes % 4 == 0) && tile_bytes <= 4 * 64;
   uint32_t* stg32 = reinterpret_cast<uint32_t*>(stg);
   auto load_words = [&](int64_t wt_, uint32_t& w0, uint32_t& w1) {
-    w0 = w1 = 0u;
-    if (wt_ < nwt) {
-      const int64_t b0 = wt_ * BPW;
-      const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
-      const int nw = (int)((nv * K * (int64_t)sizeof(IT) + 3) / 4);
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(indices + b0 * (int64_t)K);
-      if (lane < nw) w0 = __ldcs(src + lane);
-      if (lane + 32 < nw) w1 = __ldcs(src + lane + 32);
-    }
+    const int64_t b0 = wt_ * BPW;
+    const int nv = wt_ < nwt ? (int)min((int64_t)BPW, f.nblocks - b0) : 0;
+    const int nw = (int)((nv * K * (int64_t)sizeof(IT) + 3) / 4);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(indices + b0 * (int64_t)K);
+    w0 = ld_cs_u32_or0(src + lane, lane < nw);
+    w1 = ld_cs_u32_or0(src + lane + 32, lane + 32 < nw);
   };
-  uint32_t nw0 = 0, nw1 = 0;
   const int64_t wstride = (int64_t)gridDim.x * WPC;
   const double rr = radius_f64(sizeof(IT) == 1 ? BZ_I8 : (sizeof(IT) == 2 ? BZ_I16 : BZ_I32));
   const double rinv = 1.0 / rr;
-  if (words) load_words(blockIdx.x * (int64_t)WPC + w, nw0, nw1);
-  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += wstride) {
+  // the block maximum is prefetched with the words, as raw storage (the
+  // widening conversion would wait for the load on the spot)
+  using MS = typename FloatKind<FK>::T;
+  auto load_nmax = [&](int64_t wt_) -> MS {
+    const int64_t b_ = wt_ * BPW + bs;
+    const MS* src = reinterpret_cast<const MS*>(maxima) + b_;
+    const bool ok = wt_ < nwt && b_ < f.nblocks;
+    if constexpr (sizeof(MS) == 8) return __longlong_as_double((long long)ld_cs_u64_or0(src, ok));
+    else if constexpr (sizeof(MS) == 4) return __uint_as_float(ld_cs_u32_or0(src, ok));
+    else return ok ? __ldcs(src) : MS(0);
+  };
+  // two warp tiles of look-ahead: the TMA store's proxy fence waits for the
+  // lane's outstanding loads, so the loads for tile i+2 are issued after
+  // tile i's fence and consumed two tiles later
+  uint32_t pw0 = 0u, pw1 = 0u;       // tile i (next to consume)
+  uint32_t qw0 = 0u, qw1 = 0u;        // tile i + 1
+  if (words) load_words(blockIdx.x * (int64_t)WPC + w, pw0, pw1);
+  MS pn = load_nmax(blockIdx.x * (int64_t)WPC + w), qn = MS(0);
+  if (words) load_words(blockIdx.x * (int64_t)WPC + w + wstride, qw0, qw1);
+  qn = load_nmax(blockIdx.x * (int64_t)WPC + w + wstride);
+  // TST output boxes: [2][a0][a1][a2][8] per warp, after the index staging
+  constexpr int OBOX = 2 * BS;  // elements per box (two blocks)
+  TOut* obox = reinterpret_cast<TOut*>(reinterpret_cast<unsigned char*>(smem_raw) +
+                                       (size_t)WPC * BPW * XS * 8 +
+                                       ((size_t)WPC * BPW * SS * sizeof(IT) + 127) / 128 * 128) +
+               (size_t)w * 2 * OBOX;
+  // one warp tile; consumes the look-ahead registers (cw0, cw1, cn) and
+  // refills the same registers for tile wt + 2 * wstride (no register moves:
+  // a move of a pending load result would wait for it)
+  auto tile_body = [&](int64_t wt, int it, uint32_t& cw0, uint32_t& cw1, MS& cn) {
     const int64_t b = wt * BPW + bs;
     const bool valid = b < f.nblocks;
     // ---- the warp tile's kept indices -> staging
     if (words) {
       const int nw = (int)((min((int64_t)BPW, f.nblocks - wt * BPW) * K * (int64_t)sizeof(IT) + 3) / 4);
-      if (lane < nw) stg32[lane] = nw0;
-      if (lane + 32 < nw) stg32[lane + 32] = nw1;
-      load_words(wt + wstride, nw0, nw1);
+      if (lane < nw) stg32[lane] = cw0;
+      if (lane + 32 < nw) stg32[lane + 32] = cw1;
     } else {
       const int64_t b0 = wt * BPW;
       const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
       const IT* src = indices + b0 * (int64_t)K;
       for (int e = lane; e < nv * K; e += 32) stg[e] = __ldcs(src + e);
     }
-    const double nmax = valid ? load_kind<FK>(maxima, b) : 0.0;
+    const double nmax = widen_kind<FK>(cn);
     const bool odd = !(nmax >= 0x1p-900 && nmax <= 0x1p+1000);
     __syncwarp();
     double v[16];
@@ -548,7 +576,32 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
 #pragma unroll
       for (int q = 0; q < 16; ++q) v[q] = __ddiv_rn(__dmul_rn(v[q] * kUnscale, nmax), rr);
     }
-    if (valid) {
+    if constexpr (TST) {
+      TOut* box = obox + (it & 1) * OBOX;
+      if (lane == 0) tma::bulk_wait_read<1>();  // this buffer's store (two tiles ago) has read it
+      __syncwarp();
+#pragma unroll
+      for (int a0 = 0; a0 < 4; ++a0) {
+        TOut* row = box + ((a0 * 4 + i1) * 4 + i2) * 8 + bs * 4;
+#pragma unroll
+        for (int a3 = 0; a3 < 4; ++a3) row[a3] = (TOut)v[a0 * 4 + a3];
+      }
+      tma::fence_proxy_async();  // generic-proxy writes -> visible to the TMA unit
+      if (words) load_words(wt + 2 * wstride, cw0, cw1);
+      cn = load_nmax(wt + 2 * wstride);
+      __syncwarp();
+      if (lane == 0) {
+        int64_t gc[4] = {0, 0, 0, 0};
+        block_coords<4>(f, wt * BPW, gc);  // the pair's first (even) block
+        tma::store_4d(&omap, tma::smem_u32(box), (int)(gc[3] * 4), (int)(gc[2] * 4),
+                      (int)(gc[1] * 4), (int)(gc[0] * 4));
+        tma::bulk_commit();
+      }
+    } else {
+      if (words) load_words(wt + 2 * wstride, cw0, cw1);
+      cn = load_nmax(wt + 2 * wstride);
+    }
+    if (!TST && valid) {
       int64_t gc[4] = {0, 0, 0, 0};
       block_coords<4>(f, b, gc);
       const int64_t c0 = gc[0] * 4, c1 = gc[1] * 4 + i1, c2 = gc[2] * 4 + i2, c3 = gc[3] * 4;
@@ -577,6 +630,14 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
       }
     }
     __syncwarp();  // staging and exchange area reused by the next tile
+  };
+  int it = 0;
+  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += 2 * wstride, it += 2) {
+    tile_body(wt, it, pw0, pw1, pn);
+    if (wt + wstride < nwt) tile_body(wt + wstride, it + 1, qw0, qw1, qn);
+  }
+  if constexpr (TST) {
+    if (lane == 0) tma::bulk_wait_all();  // boxes read (and written) before the CTA exits
   }
 }
 
@@ -643,14 +704,25 @@ int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices
     set_error("dct4 decompress: host matrices missing");
     return BZ_E_INVALID;
   }
-  const size_t smem = (size_t)WPC * BPW * XS * 8 + (size_t)WPC * BPW * SS * index_kind_bytes(g.index_kind);
+  const size_t smem0 = (size_t)WPC * BPW * XS * 8 + (size_t)WPC * BPW * SS * index_kind_bytes(g.index_kind);
+  const int ob = out_kind == BZ_F64 ? 8 : 4;
+  // TMA box stores: block pairs never straddle a row (even grid[3]), dense
+  // 16-byte aligned output rows
+  CUtensorMap omap;
+  bool tst = false;
+  if (!getenv("BZC_B200_NO_TMA") && g.grid[3] % 2 == 0 && (g.shape[3] * ob) % 16 == 0) {
+    const uint32_t box[4] = {4, 4, 4, 8};
+    tst = tma::encode_tiled(&omap, out, ob, 4, g.shape, box, 0);
+  }
+  if (!tst) memset(&omap, 0, sizeof(omap));
+  const size_t smem = tst ? (smem0 + 127) / 128 * 128 + (size_t)WPC * 2 * (2 * BS) * ob : smem0;
 #define BZ_D(IT, FKV, TO)                                                                     \
   {                                                                                           \
-    auto kern = k_dct4_decompress<IT, FKV, TO>;                                               \
+    auto kern = tst ? k_dct4_decompress<IT, FKV, TO, true> : k_dct4_decompress<IT, FKV, TO, false>; \
     const int occ = occupancy((const void*)kern, NT, smem);                                         \
     const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));    \
     kern<<<(int)grid, NT, smem, s>>>(p, maxima, reinterpret_cast<const IT*>(indices),         \
-                                     reinterpret_cast<TO*>(out));                             \
+                                     reinterpret_cast<TO*>(out), omap);                       \
     return check_launch("dct4_decompress");                                                   \
   }
 #define BZ_O(IT, FKV)                           \

@@ -24,11 +24,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 bool encode_f32(CUtensorMap* map, const void* base, int rank, const int64_t* dims,
                 const uint32_t* box, int swizzle_bytes) {
+  return encode_tiled(map, base, 4, rank, dims, box, swizzle_bytes);
+}
+
+bool encode_tiled(CUtensorMap* map, const void* base, int elem_bytes, int rank,
+                  const int64_t* dims, const uint32_t* box, int swizzle_bytes) {
   auto fn = encode_fn();
   if (!fn || rank < 1 || rank > 5 || ((uintptr_t)base & 15)) return false;
+  if (elem_bytes != 4 && elem_bytes != 8) return false;
   cuuint64_t gdim[5], gstride[4];
   cuuint32_t bdim[5], estride[5];
-  uint64_t stride = 4;  // bytes
+  uint64_t stride = (uint64_t)elem_bytes;  // bytes
   for (int i = 0; i < rank; ++i) {  // innermost first
     const int a = rank - 1 - i;
     if (dims[a] < 1 || dims[a] > (int64_t)0xffffffff) return false;
@@ -45,7 +51,7 @@ bool encode_f32(CUtensorMap* map, const void* base, int rank, const int64_t* dim
                                 : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                 : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                       : CU_TENSOR_MAP_SWIZZLE_NONE;
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank,
+  const CUresult r = fn(map, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank,
                         const_cast<void*>(base), gdim, gstride, bdim, estride,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

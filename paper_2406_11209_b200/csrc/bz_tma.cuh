@@ -72,6 +72,26 @@ __device__ __forceinline__ void load_3d(uint32_t dst, const CUtensorMap* map, ui
       : "memory");
 }
 
+// 4-D box store of shared memory into a tensor map (bulk async group; the
+// source must stay untouched until wait_group_read says it has been read)
+__device__ __forceinline__ void store_4d(const CUtensorMap* map, uint32_t src, int c0, int c1,
+                                         int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n" ::
+          "l"(reinterpret_cast<uint64_t>(map)), "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -93,6 +113,9 @@ __device__ __forceinline__ float4 lds128f(uint32_t addr) {
 // (16-byte aligned base and strides).
 bool encode_f32(CUtensorMap* map, const void* base, int rank, const int64_t* dims,
                 const uint32_t* box, int swizzle_bytes = 128);
+// the same for float32 (elem_bytes 4) or float64 (8) elements
+bool encode_tiled(CUtensorMap* map, const void* base, int elem_bytes, int rank,
+                  const int64_t* dims, const uint32_t* box, int swizzle_bytes);
 
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
