@@ -542,8 +542,8 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": w["fk"],
             "data": "synthetic: counter-based N(0,1), partition-invariant (bz_fill_random)",
-            "config": dict(config_dict(args.workload, world, args.scaling),
-                           fast_path=bz.is_fast_path(s, shape)),
+            "config": config_dict(args.workload, world, args.scaling),  # == the reference arm's
+            "fast_path": bz.is_fast_path(s, shape),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "parity": parity,
