@@ -148,7 +148,7 @@ def sync_stream(device=None) -> None:
 
 def call(name: str, *args) -> int:
     """Call a status-returning entry point; raise NativeError on failure."""
-    lib = load_library()
+    lib = _lib if _lib is not None else load_library()  # loaded once: no per-call CUDA query
     rc = getattr(lib, name)(*args)
     if rc != 0:
         msg = lib.bz_last_error().decode(errors="replace")
@@ -178,10 +178,12 @@ def on_device(fn):
 
     @functools.wraps(fn)
     def wrapper(a, *args, **kwargs):
-        dev = _device_of(a)
-        if dev is not None and dev.type == "cuda" and dev.index is not None \
-                and dev.index != _current_device():
-            with torch.cuda.device(dev):
+        idx = getattr(a, "_dev_index", None)  # CompressedArray caches it
+        if idx is None:
+            dev = _device_of(a)
+            idx = dev.index if dev is not None and dev.type == "cuda" else None
+        if idx is not None and idx != _current_device():
+            with torch.cuda.device(idx):
                 return fn(a, *args, **kwargs)
         return fn(a, *args, **kwargs)
 

@@ -237,7 +237,8 @@ class CompressedArray:
     operand's unchanged maxima or indices (negate, mul_scalar).
     """
 
-    __slots__ = ("original_shape", "settings", "maxima", "indices", "_lay", "_dc", "_dev", "_nb")
+    __slots__ = ("original_shape", "settings", "maxima", "indices", "_lay", "_dc", "_dev", "_nb",
+                 "_didx")
 
     def __init__(self, original_shape, settings: CodecSettings, maxima, indices, *,
                  _trusted: bool = False, dc=None):
@@ -287,6 +288,16 @@ class CompressedArray:
             dev = self.indices.device
             object.__setattr__(self, "_dev", dev)
         return dev
+
+    @property
+    def _dev_index(self):
+        """CUDA device index (None for CPU tensors), cached."""
+        i = getattr(self, "_didx", None)
+        if i is None:
+            d = self.device
+            i = d.index if d.type == "cuda" else -1
+            object.__setattr__(self, "_didx", i)
+        return None if i < 0 else i
 
     @property
     def dc_plane(self) -> torch.Tensor | None:
