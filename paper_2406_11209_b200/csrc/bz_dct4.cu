@@ -453,7 +453,7 @@ k_dct4_compress_tma(const __grid_constant__ CUtensorMap xmap, const FastParams p
 // box store (4 x 4 x 4 x 8 elements) from a per-warp, double-buffered
 // shared-memory box instead of per-lane row stores with address arithmetic
 // and bounds checks (the TMA unit clips partial blocks at the array edges).
-template <typename IT, int FK, typename TOut, bool TST = false>
+template <typename IT, int FK, typename TOut, bool TST = false, bool BULK = false>
 __global__ void __launch_bounds__(256, TST ? 2 : 3)
 k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
                   const IT* __restrict__ indices, TOut* __restrict__ out,
@@ -513,39 +513,23 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
     else if constexpr (sizeof(MS) == 4) return __uint_as_float(ld_cs_u32_or0(src, ok));
     else return ok ? __ldcs(src) : MS(0);
   };
-  // two warp tiles of look-ahead: the TMA store's proxy fence waits for the
-  // lane's outstanding loads, so the loads for tile i+2 are issued after
-  // tile i's fence and consumed two tiles later
-  uint32_t pw0 = 0u, pw1 = 0u;       // tile i (next to consume)
-  uint32_t qw0 = 0u, qw1 = 0u;        // tile i + 1
-  if (words) load_words(blockIdx.x * (int64_t)WPC + w, pw0, pw1);
-  MS pn = load_nmax(blockIdx.x * (int64_t)WPC + w), qn = MS(0);
-  if (words) load_words(blockIdx.x * (int64_t)WPC + w + wstride, qw0, qw1);
-  qn = load_nmax(blockIdx.x * (int64_t)WPC + w + wstride);
+  // register look-ahead (non-BULK paths): two warp tiles ahead -- the TMA
+  // store's proxy fence waits for the lane's outstanding loads, so the loads
+  // for tile i+2 are issued after tile i's fence and consumed two tiles later
   // TST output boxes: [2][a0][a1][a2][8] per warp, after the index staging
   constexpr int OBOX = 2 * BS;  // elements per box (two blocks)
-  TOut* obox = reinterpret_cast<TOut*>(reinterpret_cast<unsigned char*>(smem_raw) +
-                                       (size_t)WPC * BPW * XS * 8 +
-                                       ((size_t)WPC * BPW * SS * sizeof(IT) + 127) / 128 * 128) +
-               (size_t)w * 2 * OBOX;
-  // one warp tile; consumes the look-ahead registers (cw0, cw1, cn) and
-  // refills the same registers for tile wt + 2 * wstride (no register moves:
-  // a move of a pending load result would wait for it)
-  auto tile_body = [&](int64_t wt, int it, uint32_t& cw0, uint32_t& cw1, MS& cn) {
+  constexpr int NBOX = BULK ? 1 : 2;  // output boxes per warp
+  TOut* obox_base = reinterpret_cast<TOut*>(reinterpret_cast<unsigned char*>(smem_raw) +
+                                            (size_t)WPC * BPW * XS * 8 +
+                                            ((size_t)WPC * BPW * SS * sizeof(IT) + 127) / 128 * 128);
+  TOut* obox = obox_base + (size_t)w * NBOX * OBOX;
+  unsigned char* bulk_base = reinterpret_cast<unsigned char*>(obox_base + (size_t)WPC * NBOX * OBOX);
+  // one block pair (warp tile) whose indices are staged in `stg`: transforms,
+  // then the output -- a TMA box store (TST) or per-lane row stores;
+  // `after_fence` issues look-ahead loads once the box is fenced
+  auto pair_body = [&](int64_t wt, int it, double nmax, auto&& after_fence) {
     const int64_t b = wt * BPW + bs;
     const bool valid = b < f.nblocks;
-    // ---- the warp tile's kept indices -> staging
-    if (words) {
-      const int nw = (int)((min((int64_t)BPW, f.nblocks - wt * BPW) * K * (int64_t)sizeof(IT) + 3) / 4);
-      if (lane < nw) stg32[lane] = cw0;
-      if (lane + 32 < nw) stg32[lane + 32] = cw1;
-    } else {
-      const int64_t b0 = wt * BPW;
-      const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
-      const IT* src = indices + b0 * (int64_t)K;
-      for (int e = lane; e < nv * K; e += 32) stg[e] = __ldcs(src + e);
-    }
-    const double nmax = widen_kind<FK>(cn);
     const bool odd = !(nmax >= 0x1p-900 && nmax <= 0x1p+1000);
     __syncwarp();
     double v[16];
@@ -577,8 +561,13 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
       for (int q = 0; q < 16; ++q) v[q] = __ddiv_rn(__dmul_rn(v[q] * kUnscale, nmax), rr);
     }
     if constexpr (TST) {
-      TOut* box = obox + (it & 1) * OBOX;
-      if (lane == 0) tma::bulk_wait_read<1>();  // this buffer's store (two tiles ago) has read it
+      // BULK: one box per warp (the previous pair's store has had a pair's
+      // compute to read it); otherwise two, alternating
+      TOut* box = obox + (NBOX == 1 ? 0 : (it & 1)) * OBOX;
+      if (lane == 0) {
+        if constexpr (BULK) tma::bulk_wait_read<0>();
+        else tma::bulk_wait_read<1>();
+      }
       __syncwarp();
 #pragma unroll
       for (int a0 = 0; a0 < 4; ++a0) {
@@ -587,8 +576,7 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
         for (int a3 = 0; a3 < 4; ++a3) row[a3] = (TOut)v[a0 * 4 + a3];
       }
       tma::fence_proxy_async();  // generic-proxy writes -> visible to the TMA unit
-      if (words) load_words(wt + 2 * wstride, cw0, cw1);
-      cn = load_nmax(wt + 2 * wstride);
+      after_fence();
       __syncwarp();
       if (lane == 0) {
         int64_t gc[4] = {0, 0, 0, 0};
@@ -598,8 +586,7 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
         tma::bulk_commit();
       }
     } else {
-      if (words) load_words(wt + 2 * wstride, cw0, cw1);
-      cn = load_nmax(wt + 2 * wstride);
+      after_fence();
     }
     if (!TST && valid) {
       int64_t gc[4] = {0, 0, 0, 0};
@@ -631,10 +618,84 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
     }
     __syncwarp();  // staging and exchange area reused by the next tile
   };
-  int it = 0;
-  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += 2 * wstride, it += 2) {
-    tile_body(wt, it, pw0, pw1, pn);
-    if (wt + wstride < nwt) tile_body(wt + wstride, it + 1, qw0, qw1, qn);
+
+  if constexpr (BULK) {
+    // ---- super tiles of 8 blocks per warp: one bulk copy of their kept
+    // indices (8 K bytes, a 16-byte multiple) and maxima into a per-warp,
+    // double-buffered shared buffer, completed on the buffer's mbarrier --
+    // no per-lane look-ahead loads (the proxy fence of the box store would
+    // wait for them)
+    constexpr int SB = 8;                                       // blocks per super tile
+    const int ib = SB * K * (int)sizeof(IT);                    // index bytes
+    constexpr int mbb = SB * (int)sizeof(MS);                   // maxima bytes
+    const int bufb = (ib + mbb + 15) / 16 * 16;
+    unsigned char* bulk = bulk_base + (size_t)w * 2 * bufb;
+    const uint32_t mb = tma::smem_u32(bulk_base + (size_t)WPC * 2 * bufb) + 16u * w;
+    if (lane == 0) {
+      tma::mbar_init(mb, 1);
+      tma::mbar_init(mb + 8, 1);
+      tma::fence_mbar_init();
+    }
+    __syncwarp();
+    const int64_t nst = f.nblocks / SB;
+    auto issue = [&](int64_t st, int buf) {
+      if (lane == 0 && st < nst) {
+        const uint32_t dst = tma::smem_u32(bulk + buf * bufb);
+        tma::mbar_arrive_expect_tx(mb + 8 * buf, (uint32_t)(ib + mbb));
+        tma::bulk_g2s(dst, indices + st * SB * (int64_t)K, (uint32_t)ib, mb + 8 * buf);
+        tma::bulk_g2s(dst + ib, reinterpret_cast<const MS*>(maxima) + st * SB, (uint32_t)mbb,
+                      mb + 8 * buf);
+      }
+    };
+    const int nw = K * (int)sizeof(IT) / 2;  // 32-bit words of a pair's indices
+    int i = 0, itb = 0;
+    int64_t st = blockIdx.x * (int64_t)WPC + w;
+    issue(st, 0);
+    for (; st < nst; st += wstride, ++i) {
+      issue(st + wstride, (i + 1) & 1);  // buffer (i+1)&1 was consumed by iteration i-1
+      tma::mbar_wait(mb + 8 * (i & 1), (uint32_t)(i >> 1) & 1u);
+      const unsigned char* buf = bulk + (i & 1) * bufb;
+      const MS* bm = reinterpret_cast<const MS*>(buf + ib);
+#pragma unroll 1
+      for (int pp = 0; pp < SB / 2; ++pp) {
+        const uint32_t* src32 = reinterpret_cast<const uint32_t*>(buf + pp * 2 * K * (int)sizeof(IT));
+        if (lane < nw) stg32[lane] = src32[lane];
+        if (lane + 32 < nw) stg32[lane + 32] = src32[lane + 32];
+        pair_body(st * (SB / 2) + pp, itb++, widen_kind<FK>(bm[2 * pp + bs]), [] {});
+      }
+    }
+  } else {
+    // one warp tile; consumes the look-ahead registers (cw0, cw1, cn) and
+    // refills the same registers for tile wt + 2 * wstride (no register
+    // moves: a move of a pending load result would wait for it)
+    auto tile_body = [&](int64_t wt, int it, uint32_t& cw0, uint32_t& cw1, MS& cn) {
+      // ---- the warp tile's kept indices -> staging
+      if (words) {
+        const int nwt_ = (int)((min((int64_t)BPW, f.nblocks - wt * BPW) * K * (int64_t)sizeof(IT) + 3) / 4);
+        if (lane < nwt_) stg32[lane] = cw0;
+        if (lane + 32 < nwt_) stg32[lane + 32] = cw1;
+      } else {
+        const int64_t b0 = wt * BPW;
+        const int nv = (int)min((int64_t)BPW, f.nblocks - b0);
+        const IT* src = indices + b0 * (int64_t)K;
+        for (int e = lane; e < nv * K; e += 32) stg[e] = __ldcs(src + e);
+      }
+      pair_body(wt, it, widen_kind<FK>(cn), [&] {
+        if (words) load_words(wt + 2 * wstride, cw0, cw1);
+        cn = load_nmax(wt + 2 * wstride);
+      });
+    };
+    uint32_t pw0 = 0u, pw1 = 0u;  // tile i (next to consume)
+    uint32_t qw0 = 0u, qw1 = 0u;  // tile i + 1
+    if (words) load_words(blockIdx.x * (int64_t)WPC + w, pw0, pw1);
+    MS pn = load_nmax(blockIdx.x * (int64_t)WPC + w);
+    if (words) load_words(blockIdx.x * (int64_t)WPC + w + wstride, qw0, qw1);
+    MS qn = load_nmax(blockIdx.x * (int64_t)WPC + w + wstride);
+    int it = 0;
+    for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += 2 * wstride, it += 2) {
+      tile_body(wt, it, pw0, pw1, pn);
+      if (wt + wstride < nwt) tile_body(wt + wstride, it + 1, qw0, qw1, qn);
+    }
   }
   if constexpr (TST) {
     if (lane == 0) tma::bulk_wait_all();  // boxes read (and written) before the CTA exits
@@ -715,10 +776,21 @@ int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices
     tst = tma::encode_tiled(&omap, out, ob, 4, g.shape, box, 0);
   }
   if (!tst) memset(&omap, 0, sizeof(omap));
-  const size_t smem = tst ? (smem0 + 127) / 128 * 128 + (size_t)WPC * 2 * (2 * BS) * ob : smem0;
+  // bulk super tiles: 8 blocks' indices a 16-byte multiple, aligned bases,
+  // whole super tiles, a pair's indices at most 64 words
+  const int ibytes = index_kind_bytes(g.index_kind);
+  const bool bulk = tst && (g.kept * ibytes) % 2 == 0 && g.kept * ibytes <= 128 &&
+                    g.nblocks % 8 == 0 && !(((uintptr_t)indices | (uintptr_t)maxima) & 15) &&
+                    !getenv("BZC_B200_NO_BULK");
+  const size_t bufb = ((size_t)8 * g.kept * ibytes + 8 * float_kind_bytes(g.float_kind) + 15) / 16 * 16;
+  const size_t smem = !tst ? smem0
+                      : bulk ? (smem0 + 127) / 128 * 128 + (size_t)WPC * (2 * BS) * ob +
+                                   (size_t)WPC * 2 * bufb + (size_t)WPC * 16
+                             : (smem0 + 127) / 128 * 128 + (size_t)WPC * 2 * (2 * BS) * ob;
 #define BZ_D(IT, FKV, TO)                                                                     \
   {                                                                                           \
-    auto kern = tst ? k_dct4_decompress<IT, FKV, TO, true> : k_dct4_decompress<IT, FKV, TO, false>; \
+    auto kern = bulk ? k_dct4_decompress<IT, FKV, TO, true, true>                             \
+                     : (tst ? k_dct4_decompress<IT, FKV, TO, true> : k_dct4_decompress<IT, FKV, TO, false>); \
     const int occ = occupancy((const void*)kern, NT, smem);                                         \
     const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));    \
     kern<<<(int)grid, NT, smem, s>>>(p, maxima, reinterpret_cast<const IT*>(indices),         \

@@ -72,6 +72,16 @@ __device__ __forceinline__ void load_3d(uint32_t dst, const CUtensorMap* map, ui
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (16-byte aligned addresses, size a multiple
+// of 16), completing as transaction bytes on `bar`
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(dst), "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 // 4-D box store of shared memory into a tensor map (bulk async group; the
 // source must stay untouched until wait_group_read says it has been read)
 __device__ __forceinline__ void store_4d(const CUtensorMap* map, uint32_t src, int c0, int c1,
