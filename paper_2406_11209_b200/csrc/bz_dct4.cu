@@ -519,9 +519,11 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
   // TST output boxes: [2][a0][a1][a2][8] per warp, after the index staging
   constexpr int OBOX = 2 * BS;  // elements per box (two blocks)
   constexpr int NBOX = BULK ? 1 : 2;  // output boxes per warp
-  TOut* obox_base = reinterpret_cast<TOut*>(reinterpret_cast<unsigned char*>(smem_raw) +
-                                            (size_t)WPC * BPW * XS * 8 +
-                                            ((size_t)WPC * BPW * SS * sizeof(IT) + 127) / 128 * 128);
+  // boxes 1024-byte aligned (the 128-byte swizzle pattern repeats every 1 KB)
+  unsigned char* obox_raw = reinterpret_cast<unsigned char*>(smem_raw) + (size_t)WPC * BPW * XS * 8 +
+                            (size_t)WPC * BPW * SS * sizeof(IT);
+  TOut* obox_base = reinterpret_cast<TOut*>(
+      obox_raw + ((1024u - (tma::smem_u32(obox_raw) & 1023u)) & 1023u));
   TOut* obox = obox_base + (size_t)w * NBOX * OBOX;
   unsigned char* bulk_base = reinterpret_cast<unsigned char*>(obox_base + (size_t)WPC * NBOX * OBOX);
   // one block pair (warp tile) whose indices are staged in `stg`: transforms,
@@ -569,11 +571,23 @@ k_dct4_decompress(const FastParams p, const void* __restrict__ maxima,
         else tma::bulk_wait_read<1>();
       }
       __syncwarp();
+      // the box is swizzled with a span of one 8-element row (64 B for f64,
+      // 32 B for f32 -- measured, tools/tma_swizzle_probe.cu: the 16-byte
+      // chunk bits [4, 4 + log2(span/16)) of the byte offset XOR bits 7..):
+      // each quarter warp's 16-byte writes land in 8 distinct bank groups
+      constexpr uint32_t SWM = 8 * sizeof(TOut) / 16 - 1;
+      unsigned char* boxb = reinterpret_cast<unsigned char*>(box);
 #pragma unroll
       for (int a0 = 0; a0 < 4; ++a0) {
-        TOut* row = box + ((a0 * 4 + i1) * 4 + i2) * 8 + bs * 4;
+        const uint32_t off = (uint32_t)((((a0 * 4 + i1) * 4 + i2) * 8 + bs * 4) * sizeof(TOut));
 #pragma unroll
-        for (int a3 = 0; a3 < 4; ++a3) row[a3] = (TOut)v[a0 * 4 + a3];
+        for (int h = 0; h < (int)sizeof(TOut) / 4; ++h) {  // 16-byte chunks of the row
+          const uint32_t o16 = off + 16u * h;
+          TOut* dst = reinterpret_cast<TOut*>(boxb + (o16 ^ (((o16 >> 7) & SWM) << 4)));
+          constexpr int PER = 16 / sizeof(TOut);
+#pragma unroll
+          for (int e = 0; e < PER; ++e) dst[e] = (TOut)v[a0 * 4 + h * PER + e];
+        }
       }
       tma::fence_proxy_async();  // generic-proxy writes -> visible to the TMA unit
       after_fence();
@@ -773,7 +787,7 @@ int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices
   bool tst = false;
   if (!getenv("BZC_B200_NO_TMA") && g.grid[3] % 2 == 0 && (g.shape[3] * ob) % 16 == 0) {
     const uint32_t box[4] = {4, 4, 4, 8};
-    tst = tma::encode_tiled(&omap, out, ob, 4, g.shape, box, 0);
+    tst = tma::encode_tiled(&omap, out, ob, 4, g.shape, box, 8 * ob);  // swizzle span = one row
   }
   if (!tst) memset(&omap, 0, sizeof(omap));
   // bulk super tiles: 8 blocks' indices a 16-byte multiple, aligned bases,
@@ -784,9 +798,9 @@ int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices
                     !getenv("BZC_B200_NO_BULK");
   const size_t bufb = ((size_t)8 * g.kept * ibytes + 8 * float_kind_bytes(g.float_kind) + 15) / 16 * 16;
   const size_t smem = !tst ? smem0
-                      : bulk ? (smem0 + 127) / 128 * 128 + (size_t)WPC * (2 * BS) * ob +
+                      : bulk ? smem0 + 1024 + (size_t)WPC * (2 * BS) * ob +
                                    (size_t)WPC * 2 * bufb + (size_t)WPC * 16
-                             : (smem0 + 127) / 128 * 128 + (size_t)WPC * 2 * (2 * BS) * ob;
+                             : smem0 + 1024 + (size_t)WPC * 2 * (2 * BS) * ob;
 #define BZ_D(IT, FKV, TO)                                                                     \
   {                                                                                           \
     auto kern = bulk ? k_dct4_decompress<IT, FKV, TO, true, true>                             \
