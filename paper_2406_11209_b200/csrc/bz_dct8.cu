@@ -38,6 +38,7 @@
 // 16-byte halves of 32-byte sectors.  Decompress runs the mirror image.
 #include "bz_fast.cuh"
 #include "bz_kernels.cuh"
+#include "bz_tma.cuh"
 
 namespace bz {
 
@@ -388,7 +389,10 @@ k_dct8_fixup(const FastParams p, const TIn* __restrict__ x, void* __restrict__ m
 }
 
 // ------------------------------------------------------------- decompress --
-template <typename IT, int FK, typename TOut>
+// BULK: each warp tile's 2 x 512 indices arrive by one bulk copy into a
+// per-warp, double-buffered shared buffer (mbarrier completion), issued one
+// tile ahead -- without it every tile waits for its own index loads.
+template <typename IT, int FK, typename TOut, bool BULK = false>
 __global__ void __launch_bounds__(256, 2)
 k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
                   const IT* __restrict__ indices, TOut* __restrict__ out) {
@@ -411,8 +415,35 @@ k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
   const int64_t s0 = f.stride[0], s1 = f.stride[1];
   const int64_t nwt = (f.nblocks + BPW - 1) / BPW;
   constexpr int PER = 16 / sizeof(IT), NU = 32 / PER;
+  const int64_t wstride = (int64_t)gridDim.x * WPC;
+  // BULK buffers after the exchange area: [warp][2][BPW * BS indices], then
+  // two mbarriers per warp
+  constexpr int TBYTES = BPW * BS * (int)sizeof(IT);
+  unsigned char* bulk = reinterpret_cast<unsigned char*>(smem_raw) + (size_t)WPC * BPW * BS * 8 +
+                        (size_t)w * 2 * TBYTES;
+  const uint32_t mb = tma::smem_u32(reinterpret_cast<unsigned char*>(smem_raw) +
+                                    (size_t)WPC * BPW * BS * 8 + (size_t)WPC * 2 * TBYTES) + 16u * w;
+  auto issue = [&](int64_t wt_, int buf) {
+    if (BULK && lane == 0 && wt_ < nwt) {
+      const int nv = (int)min((int64_t)BPW, f.nblocks - wt_ * BPW);
+      const uint32_t bytes = (uint32_t)(nv * BS * (int)sizeof(IT));
+      tma::mbar_arrive_expect_tx(mb + 8 * buf, bytes);
+      tma::bulk_g2s(tma::smem_u32(bulk + buf * TBYTES), indices + wt_ * BPW * (int64_t)BS, bytes,
+                    mb + 8 * buf);
+    }
+  };
+  if constexpr (BULK) {
+    if (lane == 0) {
+      tma::mbar_init(mb, 1);
+      tma::mbar_init(mb + 8, 1);
+      tma::fence_mbar_init();
+    }
+    __syncwarp();
+    issue(blockIdx.x * (int64_t)WPC + w, 0);
+  }
 
-  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += (int64_t)gridDim.x * WPC) {
+  int it = 0;
+  for (int64_t wt = blockIdx.x * (int64_t)WPC + w; wt < nwt; wt += wstride, ++it) {
     const int64_t b = wt * BPW + bs;
     const bool valid = b < f.nblocks;
 
@@ -421,10 +452,19 @@ k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
     double nmax;
     bool odd;
     {
-      const IT* src = indices + b * (int64_t)BS + hi * 64 + h * 32;
       uint4 r[NU];
+      if constexpr (BULK) {
+        issue(wt + wstride, (it + 1) & 1);  // buffer (it+1)&1 was consumed by the previous tile
+        tma::mbar_wait_spin(mb + 8 * (it & 1), (uint32_t)(it >> 1) & 1u);
+        const uint4* src = reinterpret_cast<const uint4*>(bulk + (it & 1) * TBYTES +
+                                                         (bs * BS + hi * 64 + h * 32) * (int)sizeof(IT));
 #pragma unroll
-      for (int u = 0; u < NU; ++u) r[u] = valid ? __ldcs(reinterpret_cast<const uint4*>(src) + u) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < NU; ++u) r[u] = valid ? src[u] : make_uint4(0, 0, 0, 0);
+      } else {
+        const IT* src = indices + b * (int64_t)BS + hi * 64 + h * 32;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) r[u] = valid ? __ldcs(reinterpret_cast<const uint4*>(src) + u) : make_uint4(0, 0, 0, 0);
+      }
       nmax = valid ? load_kind<FK>(maxima, b) : 0.0;
       odd = !(nmax >= 0x1p-900 && nmax <= 0x1p+1000);
 #pragma unroll
@@ -568,10 +608,14 @@ int launch_dct8_decompress(const Geo& g, const void* maxima, const void* indices
     set_error("dct8 decompress: host matrices missing");
     return BZ_E_INVALID;
   }
-  const size_t smem = (size_t)WPC * BPW * BS * 8;
+  const size_t smem0 = (size_t)WPC * BPW * BS * 8;
+  const int ib = index_kind_bytes(g.index_kind);
+  const bool bulk = ib <= 2 && !((uintptr_t)indices & 15) && !getenv("BZC_B200_NO_BULK");
+  const size_t smem = bulk ? smem0 + (size_t)WPC * 2 * BPW * BS * ib + (size_t)WPC * 16 : smem0;
 #define BZ_D(IT, FKV, TO)                                                                     \
   {                                                                                           \
-    auto kern = k_dct8_decompress<IT, FKV, TO>;                                               \
+    auto kern = (bulk && sizeof(IT) <= 2) ? k_dct8_decompress<IT, FKV, TO, true>              \
+                                          : k_dct8_decompress<IT, FKV, TO, false>;            \
     const int occ = occupancy((const void*)kern, NT, smem);                                         \
     const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));    \
     kern<<<(int)grid, NT, smem, s>>>(p, maxima, reinterpret_cast<const IT*>(indices),         \
