@@ -362,6 +362,9 @@ def _reduce(a, b=None, *, dc_only=False) -> Record:
     h = _host_record()
     hn = _host_record_np()
     pair = b is not None and b is not a
+    if not pair or (b.settings.index_kind is a.settings.index_kind
+                    and b._dev_index == a._dev_index):
+        return _reduce_direct(a, b if pair else None, int(dc_only), h, hn)
     if pair and b.settings.index_kind is not a.settings.index_kind:
         moments_record(a, b, dc_only=dc_only, out=h)  # widened through a device copy
         _native.sync_stream(a.device)
@@ -371,6 +374,37 @@ def _reduce(a, b=None, *, dc_only=False) -> Record:
         hn[_native.RECORD_DOUBLES - 1] = 0.0
         moments_record(a, b, dc_only=dc_only, out=h)
         _native.call("bz_wait_record", h.data_ptr(), _stream(a))
+    return Record._make(hn[:9].tolist())
+
+
+def _reduce_direct(a, b, dc_only: int, h: torch.Tensor, hn: np.ndarray) -> Record:
+    """The common case of _reduce -- one device, equal index kinds -- with the
+    fewest host steps: one library call that launches the reduction (its last
+    CTA writes the record into this thread's pinned buffer, completion flag
+    last) and one that polls the flag.  Same kernels as moments_record."""
+    lib = _native.load_library()
+    idx = a._dev_index
+    stream = _native.stream_handle(idx)
+    La = a.layout()
+    ws = _reduce_workspace(a.device, La)
+    hp = h.data_ptr()
+    hn[_native.RECORD_DOUBLES - 1] = 0.0
+    if dc_only == 1 and b is None and a._dc is not None:  # mean: the DC plane
+        rc = lib.bz_moments_dc(ctypes.byref(La), a.maxima.data_ptr(), a._dc.data_ptr(), hp,
+                               ws.data_ptr(), ws.numel(), stream)
+        name = "bz_moments_dc"
+    else:
+        Lb = b.layout() if b is not None else La
+        rc = lib.bz_moments(ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
+                            a.indices.data_ptr(), None if b is None else b.maxima.data_ptr(),
+                            None if b is None else b.indices.data_ptr(), int(b is not None),
+                            dc_only, hp, ws.data_ptr(), ws.numel(), stream)
+        name = "bz_moments"
+    if rc:
+        ws.zero_()  # never leave a half-counted ticket behind a failed launch
+        raise _native.NativeError(f"{name} failed ({rc}): "
+                                  f"{lib.bz_last_error().decode(errors='replace')}")
+    _native.call("bz_wait_record", hp, stream)
     return Record._make(hn[:9].tolist())
 
 
