@@ -491,3 +491,38 @@ def test_add_small_kernel_every_group_width(bz, keep):
     b = bz.CompressedArray(shape, s, rb.maxima, rb.indices)
     got, want = bz.subtract_l2(b, a), o.l2_norm(o.subtract(rb, ra))
     assert math.isclose(got, want, rel_tol=1e-12), (got, want)
+
+
+@pytest.mark.parametrize("shape,mask", [
+    ((14, 9, 7, 30), None),       # grid (4,3,2,8): TMA box stores + bulk super tiles, ragged edges
+    ((14, 9, 7, 30), "lowpass"),
+    ((6, 5, 3, 22), "lowpass"),   # grid (2,2,1,6): 24 blocks, TMA stores, bulk super tiles
+    ((5, 4, 4, 12), None),        # grid (2,1,1,3): odd last-axis grid -> per-lane row stores
+])
+def test_dct4_decompress_store_paths(bz, shape, mask):
+    """k_dct4_decompress paths: TMA box stores clipped at ragged array edges,
+    bulk-copied 8-block super tiles, and per-lane stores; f64 and f32 out,
+    1e-13 against the oracle on the reference's compressed data."""
+    block = (4, 4, 4, 4)
+    bits = _lowpass(block, 4) if mask == "lowpass" else None
+    x = np.random.default_rng(sum(shape)).normal(size=shape)
+    ca, ref, _ = parity(bz, x, block, "f32", "i8", mask_bits=bits)
+    s = _settings(bz, block, "f32", "i8", mask_bits=bits)
+    rc = bz.CompressedArray(x.shape, s, ref.maxima, ref.indices)
+    want = o.decompress(ref)
+    got32 = bz.decompress(rc, bz.FloatKind.F32).numpy().astype(np.float64)
+    assert np.max(np.abs(got32 - want)) <= 4e-7 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("shape", [(24, 40, 40), (16, 16, 24), (8, 8, 8)])
+def test_dct8_decompress_bulk_tiles(bz, shape):
+    """k_dct8_decompress with bulk-copied warp tiles, including an odd block
+    count (a last tile of one block) and a single block; f64 and f32 out."""
+    block = (8, 8, 8)
+    x = np.random.default_rng(sum(shape)).normal(size=shape)
+    ca, ref, _ = parity(bz, x, block, "f32", "i8")
+    s = _settings(bz, block, "f32", "i8")
+    rc = bz.CompressedArray(x.shape, s, ref.maxima, ref.indices)
+    want = o.decompress(ref)
+    got32 = bz.decompress(rc, bz.FloatKind.F32).numpy().astype(np.float64)
+    assert np.max(np.abs(got32 - want)) <= 4e-7 * np.max(np.abs(want))
