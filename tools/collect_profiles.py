@@ -32,7 +32,7 @@ OP_KERNELS = {  # bench op -> kernel name prefix
                    "k_exact_decompress"),
     "l2_norm": ("k_moments_stream", "k_moments_staged"),  # PAIR = false instantiation
     "dot": ("k_moments_stream", "k_moments_staged"),      # PAIR = true
-    "add": ("k_add", "k_add_staged"),
+    "add": ("k_add8", "k_add_small", "k_add", "k_add_staged", "k_add_tiled"),
 }
 
 STALL_KEYS = [
@@ -118,10 +118,10 @@ def main():
                     pair = len(targs) > 3 and targs[3] in ("1", "true")
                     if pair != (op == "dot"):
                         continue
-                if op == "decompress" and targs and targs[-1] != "double":
+                if op == "decompress" and targs and "double" not in targs:
                     continue  # bench "decompress" is the f64-output call
-                if any(name.split("<")[0].endswith(p) or name.startswith("void " + p) or name.startswith(p)
-                       for p in prefixes) and dram:
+                base = name.split("<")[0].split("::")[-1].split()[-1]
+                if any(base == p or base.startswith(p + "_") for p in prefixes) and dram:
                     key = f"{w}:{op}"
                     if "to_kind" not in key and key not in traffic:  # dominant kernel first
                         traffic[key] = statistics.median(dram)
