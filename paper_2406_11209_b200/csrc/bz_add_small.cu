@@ -110,7 +110,7 @@ __device__ __forceinline__ void small_prefetch(unsigned char* buf, int64_t tile,
 }
 
 template <int G, int CPL, int MODE, bool RED>
-__global__ void __launch_bounds__(256, G == 8 ? 3 : 2)
+__global__ void __launch_bounds__(256, CPL <= 24 ? 3 : 2)
 k_add_small(int64_t nblocks, int kept, const float* __restrict__ a_max,
             const int8_t* __restrict__ a_idx, const float* __restrict__ b_max,
             const int8_t* __restrict__ b_idx, int subtract, double shift,
