@@ -40,6 +40,8 @@
 #include "bz_kernels.cuh"
 #include "bz_tma.cuh"
 
+#include <cstring>
+
 namespace bz {
 
 namespace d8 {
@@ -392,13 +394,20 @@ k_dct8_fixup(const FastParams p, const TIn* __restrict__ x, void* __restrict__ m
 // BULK: each warp tile's 2 x 512 indices arrive by one bulk copy into a
 // per-warp, double-buffered shared buffer (mbarrier completion), issued one
 // tile ahead -- without it every tile waits for its own index loads.
-template <typename IT, int FK, typename TOut, bool BULK = false>
+// TST: the warp's two blocks (adjacent along x) leave as one TMA box store
+// (8 z x 8 y x 16 x) written into the warp's exchange area once phase A' has
+// read it (128-byte / 64-byte swizzled rows for f64 / f32), instead of per-lane
+// row stores with address arithmetic and bounds checks.
+template <typename IT, int FK, typename TOut, bool BULK = false, bool TST = false>
 __global__ void __launch_bounds__(256, 2)
 k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
-                  const IT* __restrict__ indices, TOut* __restrict__ out) {
+                  const IT* __restrict__ indices, TOut* __restrict__ out,
+                  const __grid_constant__ CUtensorMap omap) {
   using namespace d8;
   const FastGeo& f = p.f;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_dyn[];
+  // 1024-byte aligned base (the swizzled TMA box lives in the exchange area)
+  unsigned char* smem_raw = smem_dyn + (TST ? ((1024u - (tma::smem_u32(smem_dyn) & 1023u)) & 1023u) : 0u);
   const int t = threadIdx.x;
   const int lane = t & 31, w = t >> 5;
   const int bs = lane >> 4, o = lane & 15;
@@ -488,6 +497,10 @@ k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
         for (int e = 0; e < 32; ++e) c[e] *= scale;
       }
     }
+    if constexpr (TST) {  // the previous tile's box store has read the exchange area
+      if (lane == 0) tma::bulk_wait_read<0>();
+      __syncwarp();
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -527,7 +540,36 @@ k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
 #pragma unroll
       for (int e = 0; e < 32; ++e) v[e] = __ddiv_rn(__dmul_rn(v[e], nmax), rr);
     }
-    if (valid) {
+    if constexpr (TST) {
+      // box [z][y][16 x] in the warp's exchange area (every lane's A' reads
+      // are done: the __syncwarp above); 16-byte chunks swizzled by the row
+      // span (128 B f64: chunk ^= line & 7; 64 B f32: chunk ^= (line >> 1) & 3,
+      // i.e. byte offset bits 4.. XOR bits 7..)
+      constexpr uint32_t RB = 16 * sizeof(TOut);            // row bytes
+      constexpr uint32_t SWM = RB / 16 - 1;
+      unsigned char* box = smem_raw + (size_t)w * BPW * BS * 8;
+#pragma unroll
+      for (int z = 0; z < 8; ++z) {
+        const uint32_t off = (uint32_t)(z * 8 + hi) * RB + (uint32_t)(bs * 8 + h * 4) * sizeof(TOut);
+#pragma unroll
+        for (int q = 0; q < (int)sizeof(TOut) / 4; ++q) {  // 16-byte chunks of the 4-element row
+          const uint32_t o16 = off + 16u * q;
+          TOut* dst = reinterpret_cast<TOut*>(box + (o16 ^ (((o16 >> 7) & SWM) << 4)));
+          constexpr int PER = 16 / sizeof(TOut);
+#pragma unroll
+          for (int e = 0; e < PER; ++e) dst[e] = (TOut)v[z * 4 + q * PER + e];
+        }
+      }
+      tma::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        int64_t gc[4] = {0, 0, 0, 0};
+        block_coords<3>(f, wt * BPW, gc);  // the pair's first (even) block
+        tma::store_3d(&omap, tma::smem_u32(box), (int)(gc[2] * 8), (int)(gc[1] * 8), (int)(gc[0] * 8));
+        tma::bulk_commit();
+      }
+    }
+    if (!TST && valid) {
       int64_t gc[4] = {0, 0, 0, 0};
       block_coords<3>(f, b, gc);
       const int64_t z0 = gc[0] * 8, y = gc[1] * 8 + hi, x0 = gc[2] * 8 + h * 4;
@@ -554,6 +596,9 @@ k_dct8_decompress(const FastParams p, const void* __restrict__ maxima,
         }
       }
     }
+  }
+  if constexpr (TST) {
+    if (lane == 0) tma::bulk_wait_all();  // boxes read (and written) before the CTA exits
   }
 }
 
@@ -611,15 +656,28 @@ int launch_dct8_decompress(const Geo& g, const void* maxima, const void* indices
   const size_t smem0 = (size_t)WPC * BPW * BS * 8;
   const int ib = index_kind_bytes(g.index_kind);
   const bool bulk = ib <= 2 && !((uintptr_t)indices & 15) && !getenv("BZC_B200_NO_BULK");
-  const size_t smem = bulk ? smem0 + (size_t)WPC * 2 * BPW * BS * ib + (size_t)WPC * 16 : smem0;
+  const int ob = out_kind == BZ_F64 ? 8 : 4;
+  // TMA box stores: block pairs never straddle a row (even grid[2]), dense
+  // 16-byte aligned output rows; box = 16 x 8 x 8 elements
+  CUtensorMap omap;
+  bool tst = false;
+  if (bulk && !getenv("BZC_B200_NO_TMA") && g.grid[2] % 2 == 0 && (g.shape[2] * ob) % 16 == 0) {
+    const uint32_t box[3] = {8, 8, 16};
+    tst = tma::encode_tiled(&omap, out, ob, 3, g.shape, box, 16 * ob);  // swizzle span = one row
+  }
+  if (!tst) memset(&omap, 0, sizeof(omap));
+  const size_t smem = (bulk ? smem0 + (size_t)WPC * 2 * BPW * BS * ib + (size_t)WPC * 16 : smem0) +
+                      (tst ? 1024 : 0);
 #define BZ_D(IT, FKV, TO)                                                                     \
   {                                                                                           \
-    auto kern = (bulk && sizeof(IT) <= 2) ? k_dct8_decompress<IT, FKV, TO, true>              \
-                                          : k_dct8_decompress<IT, FKV, TO, false>;            \
+    auto kern = (bulk && sizeof(IT) <= 2)                                                     \
+                    ? (tst ? k_dct8_decompress<IT, FKV, TO, true, true>                       \
+                           : k_dct8_decompress<IT, FKV, TO, true>)                            \
+                    : k_dct8_decompress<IT, FKV, TO, false>;                                  \
     const int occ = occupancy((const void*)kern, NT, smem);                                         \
     const int64_t grid = std::min<int64_t>(p.f.ntiles, (int64_t)kSMs * std::max(occ, 1));    \
     kern<<<(int)grid, NT, smem, s>>>(p, maxima, reinterpret_cast<const IT*>(indices),         \
-                                     reinterpret_cast<TO*>(out));                             \
+                                     reinterpret_cast<TO*>(out), omap);                       \
     return check_launch("dct8_decompress");                                                   \
   }
 #define BZ_O(IT, FKV)                                   \
