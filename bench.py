@@ -288,7 +288,8 @@ class Group:
             return v
         import torch
 
-        t = torch.tensor([v], dtype=torch.float64, device=self.device)
+        dev = self.device if self.dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -298,6 +299,8 @@ class Group:
             return rec
         import torch
 
+        if self.dist.get_backend() != "nccl" and rec.is_cuda:  # --share-gpu check runs (gloo)
+            return self.gather_into(rec.cpu()).to(rec.device)
         out = torch.empty(self.world * rec.numel(), dtype=rec.dtype, device=rec.device)
         self.dist.all_gather_into_tensor(out, rec.reshape(-1))
         return out
@@ -346,10 +349,12 @@ def run_ours(args):
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
-    local = env_int("LOCAL_RANK", 0)
+    # --share-gpu (check runs only): every rank on cuda:0 over gloo, so the
+    # multi-rank path can be exercised on a one-GPU box; timings meaningless
+    local = 0 if args.share_gpu else env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    g = Group(world, rank, local, "nccl", dev)
+    g = Group(world, rank, local, "gloo" if args.share_gpu else "nccl", dev)
 
     w = WORKLOADS[args.workload]
     p = plan(args.workload, rank, world, args.scaling)
@@ -935,6 +940,8 @@ def main(argv=None):
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--dry-run", action="store_true",
                    help="rank orchestration only (CPU/gloo): plans + one max-over-ranks")
+    p.add_argument("--share-gpu", action="store_true",
+                   help="check runs: all ranks on cuda:0 over gloo (not a measurement)")
     args = p.parse_args(argv)
     args.warmup = max(3, args.warmup)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":

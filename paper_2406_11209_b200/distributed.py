@@ -48,6 +48,8 @@ def gather_records(rec: torch.Tensor, group=None) -> list[Record]:
     order (P <= 8 records -- microseconds)."""
     world = dist.get_world_size(group)
     flat = rec.contiguous().reshape(-1)
+    if dist.get_backend(group) != "nccl" and flat.is_cuda:
+        flat = flat.cpu()  # gloo moves host tensors
     out = torch.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)
     dist.all_gather_into_tensor(out, flat, group=group)
     host = out.cpu().numpy().reshape(world, -1)
@@ -57,8 +59,11 @@ def gather_records(rec: torch.Tensor, group=None) -> list[Record]:
 def allgather_sum(x: torch.Tensor, group=None) -> float:
     """Sum of one double per rank, added in rank order (deterministic)."""
     world = dist.get_world_size(group)
+    x = x.reshape(1).to(torch.float64)
+    if dist.get_backend(group) != "nccl" and x.is_cuda:
+        x = x.cpu()
     out = torch.empty(world, dtype=torch.float64, device=x.device)
-    dist.all_gather_into_tensor(out, x.reshape(1).to(torch.float64), group=group)
+    dist.all_gather_into_tensor(out, x, group=group)
     return float(sum(float(v) for v in out.cpu().numpy()))
 
 
