@@ -447,7 +447,7 @@ struct ChunkPos {
 // SPAN = false: K is a multiple of V, no chunk crosses a block boundary;
 // DC = false: no DC moments at all (keeps_first == 0 or the "sums" mode)
 template <typename IT, int NW, int U, bool PAIR, int FK, bool SPAN, bool DC = true>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, (PAIR || sizeof(IT) > 2 || FK < 0) ? 2 : 3)
 k_moments_stream(int64_t nblocks, int kept, int keeps_first, int fk_a, int fk_b,
                  const void* __restrict__ a_max, const IT* __restrict__ a_idx,
                  const void* __restrict__ b_max, const IT* __restrict__ b_idx,
