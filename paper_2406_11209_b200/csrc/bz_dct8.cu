@@ -281,11 +281,15 @@ k_dct8_compress(const FastParams p, const TIn* __restrict__ x, void* __restrict_
     // |.| operand modifier, so no instruction materialises |c|)
     // (chains start from real elements: starting from 0.0 lets the compiler
     // assume a non-negative running value and drop the |.| -- wrong results)
-    double m4[4] = {c[0], c[1], c[2], c[3]};  // four independent chains (latency)
+    // eight independent chains of three steps, then a tree (a compare-select
+    // step is a dependent DSETP -> FSEL pair: depth, not count, costs here)
+    double m8[8] = {c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]};
 #pragma unroll
-    for (int q = 4; q < 32; ++q) m4[q & 3] = fabs(c[q]) > fabs(m4[q & 3]) ? c[q] : m4[q & 3];
-    double m = fabs(m4[0]) > fabs(m4[1]) ? fabs(m4[0]) : fabs(m4[1]);
-    const double m23 = fabs(m4[2]) > fabs(m4[3]) ? fabs(m4[2]) : fabs(m4[3]);
+    for (int q = 8; q < 32; ++q) m8[q & 7] = fabs(c[q]) > fabs(m8[q & 7]) ? c[q] : m8[q & 7];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m8[k] = fabs(m8[k + 4]) > fabs(m8[k]) ? m8[k + 4] : m8[k];
+    double m = fabs(m8[0]) > fabs(m8[1]) ? fabs(m8[0]) : fabs(m8[1]);
+    const double m23 = fabs(m8[2]) > fabs(m8[3]) ? fabs(m8[2]) : fabs(m8[3]);
     m = m23 > m ? m23 : m;
 #pragma unroll
     for (int sft = 8; sft > 0; sft >>= 1) {
