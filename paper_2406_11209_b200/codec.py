@@ -49,7 +49,7 @@ class PruningMask:
     Host metadata (numpy bits); the device copy lives in the settings tables.
     """
 
-    __slots__ = ("shape", "bits", "_key")
+    __slots__ = ("shape", "bits", "_key", "_kept", "_first")
 
     def __init__(self, shape, bits):
         shape = validate_shape(shape)
@@ -60,13 +60,16 @@ class PruningMask:
         object.__setattr__(self, "shape", shape)
         object.__setattr__(self, "bits", b)
         object.__setattr__(self, "_key", (shape, b.tobytes()))
+        # immutable: the scalars every operator asks for are computed once
+        object.__setattr__(self, "_kept", int(b.sum()))
+        object.__setattr__(self, "_first", bool(b.flat[0]) if b.size else False)
 
     def __setattr__(self, name, value):
         raise AttributeError("PruningMask is immutable")
 
     @property
     def kept_count(self) -> int:
-        return int(self.bits.sum())
+        return self._kept
 
     @property
     def flat_kept(self) -> np.ndarray:
@@ -74,7 +77,7 @@ class PruningMask:
 
     @property
     def keeps_first(self) -> bool:
-        return bool(self.bits.ravel()[0])
+        return self._first
 
     @classmethod
     def full(cls, shape) -> "PruningMask":
@@ -111,7 +114,7 @@ class PruningMask:
 class CodecSettings:
     """Block shape, float kind, index kind, transform, mask (codec.py:133-179)."""
 
-    __slots__ = ("block_shape", "float_kind", "index_kind", "transform", "mask")
+    __slots__ = ("block_shape", "float_kind", "index_kind", "transform", "mask", "_bsize")
 
     def __init__(self, block_shape, float_kind: FloatKind = FloatKind.F32,
                  index_kind: IndexKind = IndexKind.I16,
@@ -126,6 +129,7 @@ class CodecSettings:
         for k, v in (("block_shape", bshape), ("float_kind", float_kind),
                      ("index_kind", index_kind), ("transform", transform), ("mask", mask)):
             object.__setattr__(self, k, v)
+        object.__setattr__(self, "_bsize", math.prod(bshape))
 
     def __setattr__(self, name, value):
         raise AttributeError("CodecSettings is immutable")
@@ -152,11 +156,11 @@ class CodecSettings:
 
     @property
     def block_size(self) -> int:
-        return int(np.prod(self.block_shape))
+        return self._bsize
 
     @property
     def block_mean_scale(self) -> float:
-        return float(np.sqrt(self.block_size))
+        return math.sqrt(self._bsize)  # correctly rounded, as np.sqrt
 
     def grid_for(self, shape) -> tuple[int, ...]:
         shape = validate_shape(shape)

@@ -359,8 +359,10 @@ def _reduce(a, b=None, *, dc_only=False) -> Record:
     hook = getattr(a, "_reduce_record", None)
     if hook is not None:
         return hook(b, dc_only)
-    h = _host_record()
-    hn = _host_record_np()
+    try:
+        h, hn = _TLS.rec, _TLS.rec_np
+    except AttributeError:
+        h, hn = _host_record(), _host_record_np()
     pair = b is not None and b is not a
     if not pair or (b.settings.index_kind is a.settings.index_kind
                     and b._dev_index == a._dev_index):
@@ -382,11 +384,13 @@ def _reduce_direct(a, b, dc_only: int, h: torch.Tensor, hn: np.ndarray) -> Recor
     fewest host steps: one library call that launches the reduction (its last
     CTA writes the record into this thread's pinned buffer, completion flag
     last) and one that polls the flag.  Same kernels as moments_record."""
-    lib = _native.load_library()
+    lib = _native._lib if _native._lib is not None else _native.load_library()
     idx = a._dev_index
-    stream = _native.stream_handle(idx)
+    stream = _native._raw_stream(idx)
     La = a.layout()
-    ws = _reduce_workspace(a.device, La)
+    ws = _REDUCE_WS.get((idx, stream))
+    if ws is None or ws.numel() < _MOMENTS_WS_BYTES[0]:
+        ws = _reduce_workspace(a.device, La)
     hp = h.data_ptr()
     hn[_native.RECORD_DOUBLES - 1] = 0.0
     if dc_only == 1 and b is None and a._dc is not None:  # mean: the DC plane

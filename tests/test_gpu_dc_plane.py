@@ -62,6 +62,10 @@ CASES = [
     ((256, 192), (4, 4), "f64", "i16", None),             # exact fused 2-D (+ gather)
     ((24, 20, 12), (4, 4, 4), "f64", "i32", None),        # generic / other fused
     ((64, 48), (8, 8), "f32", "i16", 3),                  # pruned 2-D mask keeping DC
+    # float64 maxima over >= 4096 blocks: the bulk-copied plane kernel
+    # (69077 / 8385 blocks: ragged multi-stage CTA ranges plus a tail < 16)
+    ((4 * 67, 4 * 1031), (4, 4), "f64", "i16", None),
+    ((4 * 65, 4 * 129), (4, 4), "f64", "i32", None),
 ]
 
 

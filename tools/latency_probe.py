@@ -63,5 +63,43 @@ def main(name):
     pstats.Stats(pr).sort_stats("tottime").print_stats(14)
 
 
+def mean_breakdown(name="c3"):
+    """Where mean(api) spends its time: the public call, the direct reduce,
+    the two raw library calls, and the floor of one tiny launch + flag wait."""
+    import ctypes
+    shape, block, fk, ik, _ = CONFIGS[name]
+    s = bz.CodecSettings(block, bz.FloatKind(fk), bz.IndexKind(ik))
+    ca = bz.compress(fill(shape, bz.FloatKind(fk), 1), s)
+    lib = bz._native.load_library()
+    h = ops._host_record()
+    hn = ops._host_record_np()
+    La = ca.layout()
+    ws = ops._reduce_workspace(ca.device, La)
+    stream = bz._native.stream_handle(ca._dev_index)
+    hp = h.data_ptr()
+
+    def raw():
+        hn[15] = 0.0
+        lib.bz_moments_dc(ctypes.byref(La), ca.maxima.data_ptr(), ca._dc.data_ptr(), hp,
+                          ws.data_ptr(), ws.numel(), stream)
+        lib.bz_wait_record(ctypes.c_void_p(hp), ctypes.c_void_p(stream))
+
+    def launch_only():
+        lib.bz_moments_dc(ctypes.byref(La), ca.maxima.data_ptr(), ca._dc.data_ptr(), hp,
+                          ws.data_ptr(), ws.numel(), stream)
+
+    print(f"== mean breakdown {name}")
+    print(f"  mean (public)           {wall(lambda: bz.mean(ca), 2000):8.1f} us")
+    print(f"  _reduce_direct          {wall(lambda: ops._reduce_direct(ca, None, 1, h, hn), 2000):8.1f} us")
+    print(f"  raw launch + wait       {wall(raw, 2000):8.1f} us")
+    print(f"  raw launch only (host)  {wall(launch_only, 2000):8.1f} us")
+    print(f"  plane kernel (events)   {timeit(lambda: ops.moments_record(ca, dc_only=1), 50) * 1e3:8.1f} us")
+
+
+
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "c2")
+    if os.environ.get("MEAN_BREAKDOWN"):
+        mean_breakdown(os.environ["MEAN_BREAKDOWN"])
+    else:
+        main(sys.argv[1] if len(sys.argv) > 1 else "c2")
+
