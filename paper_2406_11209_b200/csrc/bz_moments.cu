@@ -341,18 +341,24 @@ __device__ __forceinline__ void seg_sums(SegSums<IT>& s, const Chunk<NW>& a, con
         if (PAIR) { ab0 = __dp4a((int)a.w[w], (int)b.w[w], ab0); b0 = __dp4a((int)b.w[w], (int)b.w[w], b0); }
       }
     } else {  // branch-free two-segment split (p >= V: the mask is all ones)
+      // whole-chunk sums and segment-0 sums (x & m) * y; segment 1 is the
+      // difference.  Word w's byte mask covers its bytes below p: the low
+      // 8 (p - 4w) bits, clamped to [0, 32] -- one clamped funnel shift
+      int ta = 0, tab = 0, tb = 0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
-        const unsigned m = word_mask(p, w);
-        const int la = (int)(a.w[w] & m), ha = (int)(a.w[w] & ~m);
-        a0 = __dp4a(la, la, a0);
-        a1 = __dp4a(ha, ha, a1);
+        const unsigned m = __funnelshift_lc(0xffffffffu, 0u, (unsigned)max(8 * p - 32 * w, 0));
+        const int xa = (int)a.w[w], la = (int)(a.w[w] & m);
+        ta = __dp4a(xa, xa, ta);
+        a0 = __dp4a(la, xa, a0);
         if (PAIR) {
-          const int lb = (int)(b.w[w] & m), hb = (int)(b.w[w] & ~m);
-          ab0 = __dp4a(la, lb, ab0); b0 = __dp4a(lb, lb, b0);
-          ab1 = __dp4a(ha, hb, ab1); b1 = __dp4a(hb, hb, b1);
+          const int xb = (int)b.w[w], lb = (int)(b.w[w] & m);
+          tab = __dp4a(xa, xb, tab); tb = __dp4a(xb, xb, tb);
+          ab0 = __dp4a(la, xb, ab0); b0 = __dp4a(lb, xb, b0);
         }
       }
+      a1 = ta - a0;
+      if (PAIR) { ab1 = tab - ab0; b1 = tb - b0; }
     }
     s.aa[0] = a0; s.ab[0] = ab0; s.bb[0] = b0;
     s.aa[1] = a1; s.ab[1] = ab1; s.bb[1] = b1;
