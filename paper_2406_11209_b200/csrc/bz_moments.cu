@@ -315,7 +315,11 @@ __device__ __forceinline__ Chunk<NW> ld_chunk(const void* p) {
 
 template <typename IT>
 struct SegSums {
-  using T = typename std::conditional<(sizeof(IT) <= 2), long long, double>::type;
+  // int8: a segment's products stay below 32 * 127^2 -- 32-bit integer sums
+  // and conversions (no 64-bit multiply / I2F.S64 per chunk)
+  using T = typename std::conditional<
+      sizeof(IT) == 1, int,
+      typename std::conditional<(sizeof(IT) <= 2), long long, double>::type>::type;
   T ab[2] = {0, 0}, aa[2] = {0, 0}, bb[2] = {0, 0};
 };
 
@@ -434,7 +438,8 @@ __device__ __forceinline__ double ld_max(const void* p, int64_t i, int fk) {
 
 template <typename IT>
 __device__ __forceinline__ typename SegSums<IT>::T sprod(long long x, long long y) {
-  if constexpr (sizeof(IT) <= 2) return x * y;
+  if constexpr (sizeof(IT) == 1) return (int)x * (int)y;
+  else if constexpr (sizeof(IT) <= 2) return x * y;
   else return (double)x * (double)y;
 }
 

@@ -27,6 +27,16 @@ def main(name, reps=2):
     y = fill(shape, kind, 2)
     ca = bz.compress(x, s)
     cb = bz.compress(y, s)
+    only = os.environ.get("PROFILE_ONLY")  # one op: l2 | dot | cov | mean
+    if only:
+        ops = {"l2": lambda: bz.ops.moments_record(ca, dc_only=2),
+               "dot": lambda: bz.ops.moments_record(ca, cb, dc_only=2),
+               "cov": lambda: bz.ops.moments_record(ca, cb),
+               "mean": lambda: bz.ops.moments_record(ca, dc_only=True)}
+        for _ in range(reps):
+            ops[only]()
+        torch.cuda.synchronize()
+        return
     for _ in range(reps):
         bz.compress(x, s)
         bz.decompress(ca)
