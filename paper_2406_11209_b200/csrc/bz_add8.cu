@@ -237,14 +237,29 @@ bool add8_supported(const Geo& ga, const Geo& gb, int mode, const void* a_idx, c
   return (al & 15) == 0;
 }
 
+// lanes per block: on large arrays, blocks of more than 256 kept give each
+// lane two 16-byte chunks (GS = 16 at K = 512: the per-block work -- t_hi /
+// t_lo, the 5-round shuffle maximum, bin_ctx -- is shared by twice the
+// coefficients; C3 add 1.16 -> 1.03 ms, subtract+l2 1.19 -> 1.08 ms).
+// Small arrays (C1: 32768 blocks, 34 vs 51 us) and smaller blocks keep one
+// chunk per lane and 3 CTAs per SM.
+static int add8_group(int vecs, int64_t nblocks) {
+  int GS = 1;
+  if (vecs > 16 && nblocks >= (int64_t{1} << 18)) {
+    while (GS < 32 && 2 * GS < vecs) GS <<= 1;
+  } else {
+    while (GS < 32 && GS < vecs) GS <<= 1;
+  }
+  return GS;
+}
+
 int launch_add8(const Geo& ga, const void* a_max, const void* a_idx, const void* b_max,
                 const void* b_idx, int subtract, double shift, int mode, void* out_max,
                 void* out_idx, cudaStream_t s, void* out_dc) {
   const int vecs = ga.kept / 16;
-  int GS = 1;
-  while (GS < 32 && GS < vecs) GS <<= 1;
+  const int GS = add8_group(vecs, ga.nblocks);
   const int NCH = (vecs + GS - 1) / GS;  // 1 or 2
-  const int grid = grid_for(ga.nblocks * GS, 256, 3);
+  const int grid = grid_for(ga.nblocks * GS, 256, NCH == 1 ? 3 : 2);
 #define BZ_A8(G, N, M)                                                                        \
   k_add8<G, N, M><<<grid, 256, 0, s>>>(ga.nblocks, ga.kept, (const float*)a_max,              \
                                        (const int8_t*)a_idx, (const float*)b_max,             \
@@ -270,10 +285,9 @@ int launch_subtract_l2_add8(const Geo& ga, const void* a_max, const void* a_idx,
                             const void* b_max, const void* b_idx, double* red_ws, double* out,
                             cudaStream_t s) {
   const int vecs = ga.kept / 16;
-  int GS = 1;
-  while (GS < 32 && GS < vecs) GS <<= 1;
+  const int GS = add8_group(vecs, ga.nblocks);
   const int NCH = (vecs + GS - 1) / GS;  // 1 or 2
-  const int grid = grid_for(ga.nblocks * GS, 256, 3);
+  const int grid = grid_for(ga.nblocks * GS, 256, NCH == 1 ? 3 : 2);
 #define BZ_R8(G, N)                                                                           \
   k_add8<G, N, 0, true><<<grid, 256, 0, s>>>(ga.nblocks, ga.kept, (const float*)a_max,        \
                                              (const int8_t*)a_idx, (const float*)b_max,       \

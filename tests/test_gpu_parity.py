@@ -526,3 +526,70 @@ def test_dct8_decompress_bulk_tiles(bz, shape):
     want = o.decompress(ref)
     got32 = bz.decompress(rc, bz.FloatKind.F32).numpy().astype(np.float64)
     assert np.max(np.abs(got32 - want)) <= 4e-7 * np.max(np.abs(want))
+
+
+def _random_compressed(rng, grid, kept, scale=1.0):
+    """Synthetic int8 / float32 compressed blocks: indices in [-127, 127]
+    with one +-127 per block (a valid binning), float32 maxima."""
+    nb = int(np.prod(grid))
+    idx = rng.integers(-126, 127, size=(nb, kept), dtype=np.int8)
+    pos = rng.integers(0, kept, size=nb)
+    idx[np.arange(nb), pos] = np.where(rng.random(nb) < 0.5, -127, 127).astype(np.int8)
+    mx = (scale * np.exp(rng.normal(size=nb))).astype(np.float32).astype(np.float64)
+    return mx.reshape(grid), idx.reshape(tuple(grid) + (kept,))
+
+
+@pytest.mark.parametrize("block,keep", [((8, 8, 16), 1024), ((8, 8, 16), 768)])
+def test_add8_two_chunks_per_lane(bz, block, keep):
+    """bz_add8.cu with blocks of more than 512 kept (two 16-byte chunks per
+    lane, 32 lanes per block): add / subtract / add_scalar vs the oracle."""
+    rng = np.random.default_rng(17)
+    bits = np.zeros(int(np.prod(block)), bool)
+    bits[0] = True
+    bits[1 + rng.permutation(bits.size - 1)[:keep - 1]] = True
+    bits = bits.reshape(block)
+    s = _settings(bz, block, "f32", "i8", mask_bits=bits)
+    os_ = o.Settings(block, "f32", "i8", "dct", bits)
+    grid = (3, 4, 5)
+    shape = tuple(b * g for b, g in zip(block, grid))
+    ma, ia = _random_compressed(rng, grid, keep)
+    mb, ib = _random_compressed(rng, grid, keep, scale=0.5)
+    ra, rb = o.Compressed(shape, os_, ma, ia), o.Compressed(shape, os_, mb, ib)
+    a = bz.CompressedArray(shape, s, ma.astype(np.float32), ia)
+    b = bz.CompressedArray(shape, s, mb.astype(np.float32), ib)
+    for got, want in ((bz.add(a, b), o.add(ra, rb)), (bz.subtract(a, b), o.subtract(ra, rb)),
+                      (bz.add_scalar(a, 0.25), o.add_scalar(ra, 0.25))):
+        assert np.array_equal(got.maxima_f64().cpu().numpy(), want.maxima)
+        assert np.array_equal(got.indices.cpu().numpy(), want.indices)
+    got, want = bz.subtract_l2(a, b), o.l2_norm(o.subtract(ra, rb))
+    assert math.isclose(got, want, rel_tol=1e-12), (got, want)
+
+
+def test_add8_large_array_group_width(bz):
+    """Arrays of >= 2^18 blocks of 512 int8 (the C3 shape class) run add8
+    with 16 lanes per block and two chunks per lane: a random sample of
+    blocks is checked against the oracle block by block (the operators are
+    block-local), and the fused subtract + l2 against l2_norm(subtract)."""
+    rng = np.random.default_rng(23)
+    block, keep = (8, 8, 8), 512
+    grid = (64, 64, 64)  # 262144 blocks
+    shape = tuple(b * g for b, g in zip(block, grid))
+    s = _settings(bz, block, "f32", "i8")
+    ma, ia = _random_compressed(rng, grid, keep)
+    mb, ib = _random_compressed(rng, grid, keep, scale=2.0)
+    a = bz.CompressedArray(shape, s, ma.astype(np.float32), ia)
+    b = bz.CompressedArray(shape, s, mb.astype(np.float32), ib)
+    sample = np.sort(rng.choice(int(np.prod(grid)), size=1500, replace=False))
+    os_ = o.Settings(block, "f32", "i8")
+    sub_shape = (8 * sample.size, 8, 8)
+    pick = lambda m, i: (m.reshape(-1)[sample].reshape(-1, 1, 1),
+                         i.reshape(-1, keep)[sample].reshape(-1, 1, 1, keep))
+    ra = o.Compressed(sub_shape, os_, *pick(ma, ia))
+    rb = o.Compressed(sub_shape, os_, *pick(mb, ib))
+    for got, want in ((bz.add(a, b), o.add(ra, rb)), (bz.subtract(a, b), o.subtract(ra, rb))):
+        gm = got.maxima_f64().cpu().numpy().reshape(-1)[sample]
+        gi = got.indices.cpu().numpy().reshape(-1, keep)[sample]
+        assert np.array_equal(gm, want.maxima.reshape(-1))
+        assert np.array_equal(gi, want.indices.reshape(-1, keep))
+    fused, ref = bz.subtract_l2(a, b), bz.l2_norm(bz.subtract(a, b))
+    assert math.isclose(fused, ref, rel_tol=1e-12), (fused, ref)
