@@ -210,7 +210,8 @@ int bz_approx_wasserstein(const bz_layout* La, const bz_layout* Lb, const void* 
 /* Fused time-series step (cli.py:240-243): the squared L2 norm of
  * subtract(a, b) = add(a, negate(b)) -- sum over blocks of N^2 * sum q^2 with
  * the rebinned q, N of the difference, bit-identical to materialising it --
- * written to out[0] (device double) without writing the difference.  Returns
+ * written to out[0] (a device double, or pinned host memory under UVA: the
+ * last CTA stores it) without writing the difference.  Returns
  * BZ_E_UNSUPPORTED for configurations without a fused kernel (other index
  * kinds, mixed float kinds, unaligned indices): compose bz_add + bz_moments.
  * ws: bz_subtract_l2_workspace() bytes, zeroed before first use. */

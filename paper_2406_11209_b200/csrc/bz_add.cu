@@ -125,13 +125,21 @@ __device__ __forceinline__ void st_max(void* p, int64_t i, double v, int fk) {
 // sum (q * N)^2 = sum_blocks N^2 * sum q^2 (exact integer block sums) and
 // reduce it deterministically into red_ws[1] (the fused time-series step
 // l2_norm(add(s[i+1], negate(s[i]))), cli.py:240-243, in one pass).
+// CTAs per SM: 3 (85 registers) by default; the 16-bit two-chunk blocks (C2's
+// 4x4 I16) hold 16 f64 coefficients plus the next block's 64 bytes in flight
+// per lane, which at 85 registers spilled the prefetch registers (the spill
+// store waited on the pending load): 2 CTAs, 128 registers.
+template <typename IT, int NCH>
+constexpr int add_ctas() { return (sizeof(IT) == 2 && NCH == 2) ? 2 : 3; }
+
 template <typename IT, int GS, int NCH, bool VEC, int FK, int MODE, bool RED = false>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, add_ctas<IT, NCH>())
 k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
       const void* __restrict__ a_max, const IT* __restrict__ a_idx,
       const void* __restrict__ b_max, const IT* __restrict__ b_idx, int subtract,
       double shift, int mode_rt, void* __restrict__ out_max, IT* __restrict__ out_idx,
-      double* __restrict__ red_ws = nullptr, IT* __restrict__ out_dc = nullptr) {
+      double* __restrict__ red_ws = nullptr, IT* __restrict__ out_dc = nullptr,
+      double* __restrict__ red_out = nullptr) {
   double red_acc = 0.0;
   constexpr int mode = MODE;
   (void)mode_rt;
@@ -312,7 +320,7 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
     }
     if (RED) red_acc = __fma_rn((double)red_sq * n, n, red_acc);
   }
-  if constexpr (RED) red_finish(red_acc, red_ws);
+  if constexpr (RED) red_finish(red_acc, red_ws, red_out);
 }
 
 // --------------------------------------- staged add (unaligned blocks) --
@@ -464,7 +472,7 @@ k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
             const IT* __restrict__ a_idx, const void* __restrict__ b_max,
             const IT* __restrict__ b_idx, int subtract, double shift,
             void* __restrict__ out_max, IT* __restrict__ out_idx,
-            double* __restrict__ red_ws = nullptr) {
+            double* __restrict__ red_ws = nullptr, double* __restrict__ red_out = nullptr) {
   double red_acc = 0.0;
   constexpr int IK = sizeof(IT) == 1 ? BZ_I8 : BZ_I16;
   using MT = typename std::conditional<FK == BZ_F64, double, float>::type;
@@ -610,7 +618,7 @@ k_add_tiled(int64_t nblocks, int kept, int tb, const void* __restrict__ a_max,
     if (!RED) smem_to_tile(reinterpret_cast<unsigned char*>(out_idx) + byte0, so, nbytes, miso, t, 256);
     __syncthreads();  // tiles reused
   }
-  if constexpr (RED) red_finish(red_acc, red_ws);
+  if constexpr (RED) red_finish(red_acc, red_ws, red_out);
 }
 
 template <typename IT>
@@ -658,7 +666,8 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
   const bool vec = ((kept * sizeof(IT)) % 16 == 0) &&
                    !(((uintptr_t)a_idx | (uintptr_t)out_idx | (mode == 0 ? (uintptr_t)b_idx : 0)) & 15);
   const int64_t threads = ga.nblocks * GS;
-  const int grid = grid_for(threads, 256, 3);  // persistent: 3 CTAs per SM
+  // persistent: add_ctas<IT, NCH>() CTAs per SM
+  const int grid = grid_for(threads, 256, (sizeof(IT) == 2 && NCH == 2) ? 2 : 3);
   const bool same_fk = ga.float_kind == gb.float_kind || mode != 0;
   // unaligned blocks of I8 / I16 indices: shared-memory staged tiles
   if constexpr (sizeof(IT) <= 2) {
@@ -679,7 +688,7 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
     const int occ = occupancy((const void*)kern, 256, smem);                                        \
     const int g2 = (int)std::min<int64_t>(ntiles, (int64_t)kSMs * std::max(occ, 1));                \
     kern<<<g2, 256, smem, s>>>(ga.nblocks, kept, tbt, a_max, (const IT*)a_idx, b_max,               \
-                               (const IT*)b_idx, subtract, shift, out_max, (IT*)out_idx, nullptr);  \
+                               (const IT*)b_idx, subtract, shift, out_max, (IT*)out_idx, nullptr, nullptr); \
     return check_launch("add_tiled");                                                               \
   }
 #define BZ_TC(F, M)                                                     \
@@ -750,6 +759,8 @@ static int launch_add_t(const Geo& ga, const Geo& gb, const void* a_max, const v
 // fused l2_norm(subtract(a, b)): the k_add RED variant; ws (zeroed once,
 // re-armed by the kernel) holds [counter, result, CTA partials]; the sum of
 // squares lands in ws[1] and is copied to `out`
+__global__ void k_store_zero(double* out) { *out = 0.0; }
+
 size_t subtract_l2_workspace() { return (size_t)(2 + kSMs * 3) * sizeof(double); }
 
 template <typename IT>
@@ -785,7 +796,7 @@ static int launch_subtract_l2_t(const Geo& ga, const Geo& gb, const void* a_max,
     const int occ = occupancy((const void*)kern, 256, smem);                                        \
     const int g2 = (int)std::min<int64_t>(ntiles, (int64_t)kSMs * std::min(std::max(occ, 1), 3));   \
     kern<<<g2, 256, smem, s>>>(ga.nblocks, kept, tbt, a_max, (const IT*)a_idx, b_max,               \
-                               (const IT*)b_idx, 1, 0.0, nullptr, nullptr, ws);                     \
+                               (const IT*)b_idx, 1, 0.0, nullptr, nullptr, ws, out);                \
   }
 #define BZ_TC(F)                                                            \
   {                                                                         \
@@ -799,21 +810,18 @@ static int launch_subtract_l2_t(const Geo& ga, const Geo& gb, const void* a_max,
     if (ga.float_kind == BZ_F64) BZ_TC(BZ_F64) else BZ_TC(BZ_F32)
 #undef BZ_TC
 #undef BZ_TT
-    if (int rc = check_launch("subtract_l2_tiled")) return rc;
-    if (cudaMemcpyAsync(out, ws + 1, sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-      return check_launch("subtract_l2 copy");
-    return BZ_OK;
+    return check_launch("subtract_l2_tiled");
   }
   if (!vec || ga.float_kind != gb.float_kind ||
       (ga.float_kind != BZ_F32 && ga.float_kind != BZ_F64))
     return BZ_E_UNSUPPORTED;
-  const int grid = grid_for(ga.nblocks * GS, 256, 3);
+  const int grid = grid_for(ga.nblocks * GS, 256, (sizeof(IT) == 2 && NCH == 2) ? 2 : 3);
 #define BZ_R(G, N, F)                                                                          \
   k_add<IT, G, N, true, F, 0, true><<<grid, 256, 0, s>>>(ga.nblocks, kept, ga.float_kind,       \
                                                          gb.float_kind, ga.float_kind, a_max,   \
                                                          (const IT*)a_idx, b_max,               \
                                                          (const IT*)b_idx, 1, 0.0, 0, nullptr,  \
-                                                         nullptr, ws)
+                                                         nullptr, ws, nullptr, out)
 #define BZ_RF(G, N) \
   do { if (ga.float_kind == BZ_F64) BZ_R(G, N, BZ_F64); else BZ_R(G, N, BZ_F32); } while (0)
 #define BZ_RG(G)                               \
@@ -826,17 +834,17 @@ static int launch_subtract_l2_t(const Geo& ga, const Geo& gb, const void* a_max,
 #undef BZ_RG
 #undef BZ_RF
 #undef BZ_R
-  if (int rc = check_launch("subtract_l2")) return rc;
-  if (cudaMemcpyAsync(out, ws + 1, sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-    return check_launch("subtract_l2 copy");
-  return BZ_OK;
+  return check_launch("subtract_l2");
 }
 
 int launch_subtract_l2(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                        const void* b_max, const void* b_idx, double* out, void* ws,
                        size_t ws_bytes, cudaStream_t s) {
   if (ws_bytes < subtract_l2_workspace()) { set_error("subtract_l2: workspace too small"); return BZ_E_WORKSPACE; }
-  if (ga.nblocks == 0 || ga.kept == 0) return cudaMemsetAsync(out, 0, sizeof(double), s) == cudaSuccess ? BZ_OK : BZ_E_CUDA;
+  if (ga.nblocks == 0 || ga.kept == 0) {  // out may be pinned host memory: a store, not a memset
+    k_store_zero<<<1, 1, 0, s>>>(out);
+    return check_launch("subtract_l2 empty");
+  }
   double* w = reinterpret_cast<double*>(ws);
   if (add_small_supported(ga, gb, 0, a_max, a_idx, b_max, b_idx, nullptr))  // bz_add_small.cu
     return launch_subtract_l2_small(ga, a_max, a_idx, b_max, b_idx, w, out, s);

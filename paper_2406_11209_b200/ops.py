@@ -582,16 +582,20 @@ def _subtract_l2_sq(a: CompressedArray, b: CompressedArray, out: torch.Tensor) -
 def subtract_l2(a: CompressedArray, b: CompressedArray) -> float:
     """l2_norm(subtract(a, b)) in one fused pass (cli.py:240-243); the same
     value as materialising the difference (rebinned under a's settings)."""
-    out = torch.empty(1, dtype=torch.float64, device=a.device)
     sharded = getattr(a, "_reduce_sum", None)
     if sharded is not None:
         # each shard's fused squared norm, summed across ranks in rank order
+        out = torch.empty(1, dtype=torch.float64, device=a.device)
         if not _subtract_l2_sq(a, b, out):
             return l2_norm(subtract(a, b))
         return float(math.sqrt(max(sharded(out), 0.0))) / _radius(a)
-    if not _subtract_l2_sq(a, b, out):
+    # the kernel's last CTA stores the sum straight into this thread's pinned
+    # record buffer; wait on the stream, no device scalar and no .item()
+    h = _host_record()
+    if not _subtract_l2_sq(a, b, h):
         return l2_norm(subtract(a, b))
-    return float(math.sqrt(max(float(out.item()), 0.0))) / _radius(a)
+    _native.sync_stream(a.device)
+    return float(math.sqrt(max(float(_host_record_np()[0]), 0.0))) / _radius(a)
 
 
 def timeseries_distances(snapshots, measure: str = "l2", p: float = 1.0) -> list:

@@ -32,7 +32,10 @@ def main(name, reps=2):
         ops = {"l2": lambda: bz.ops.moments_record(ca, dc_only=2),
                "dot": lambda: bz.ops.moments_record(ca, cb, dc_only=2),
                "cov": lambda: bz.ops.moments_record(ca, cb),
-               "mean": lambda: bz.ops.moments_record(ca, dc_only=True)}
+               "mean": lambda: bz.ops.moments_record(ca, dc_only=True),
+               "add": lambda: bz.add(ca, cb),
+               "sub_l2": lambda: bz.ops._subtract_l2_sq(
+                   ca, cb, torch.empty(1, dtype=torch.float64, device=ca.device))}
         for _ in range(reps):
             ops[only]()
         torch.cuda.synchronize()
