@@ -200,6 +200,12 @@ int bz_fill_random(void* out, int kind, int64_t n, int64_t offset, uint64_t seed
  * reference's IEEE op order, row-major grid order, into out[nblocks] (f64). */
 int bz_block_means(const bz_layout* L, const void* maxima, const void* indices, double* out,
                    void* stream);
+/* block_means from the DC plane (indices[..., 0] stored contiguously, one
+ * index per block -- the plane the compress / add kernels write): the same
+ * values as bz_block_means, reading B*(idx+f) bytes instead of a K-strided
+ * gather. */
+int bz_block_means_dc(const bz_layout* L, const void* maxima, const void* dc, double* out,
+                      void* stream);
 /* approx_wasserstein (ops.py:362-384) entirely on the device: block means,
  * softmax where |sum - 1| > tol, radix sort, (mean |d|^order)^(1/order)
  * into result[0] (device f64).  ws: bz_wasserstein_workspace(La) bytes. */
@@ -207,6 +213,12 @@ size_t bz_wasserstein_workspace(const bz_layout* L);
 int bz_approx_wasserstein(const bz_layout* La, const bz_layout* Lb, const void* a_max,
                           const void* a_idx, const void* b_max, const void* b_idx, double order,
                           double tol, double* result, void* ws, size_t ws_bytes, void* stream);
+/* The same with the operands' DC planes (a_dc / b_dc; nullptr = gather the
+ * first coefficients from a_idx / b_idx). */
+int bz_approx_wasserstein_dc(const bz_layout* La, const bz_layout* Lb, const void* a_max,
+                             const void* a_idx, const void* a_dc, const void* b_max,
+                             const void* b_idx, const void* b_dc, double order, double tol,
+                             double* result, void* ws, size_t ws_bytes, void* stream);
 /* Fused time-series step (cli.py:240-243): the squared L2 norm of
  * subtract(a, b) = add(a, negate(b)) -- sum over blocks of N^2 * sum q^2 with
  * the rebinned q, N of the difference, bit-identical to materialising it --

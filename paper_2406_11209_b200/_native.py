@@ -90,8 +90,10 @@ SIGNATURES = {
     "bz_convert_indices": (_I, [_P, _I, _P, _I, _I64, _P]),
     "bz_fill_random": (_I, [_P, _I, _I64, _I64, ctypes.c_uint64, _I, _P]),
     "bz_block_means": (_I, [_L, _P, _P, _P, _P]),
+    "bz_block_means_dc": (_I, [_L, _P, _P, _P, _P]),
     "bz_wasserstein_workspace": (_SZ, [_L]),
     "bz_approx_wasserstein": (_I, [_L, _L, _P, _P, _P, _P, _D, _D, _P, _P, _SZ, _P]),
+    "bz_approx_wasserstein_dc": (_I, [_L, _L, _P, _P, _P, _P, _P, _P, _D, _D, _P, _P, _SZ, _P]),
     "bz_subtract_l2_workspace": (_SZ, []),
     "bz_subtract_l2": (_I, [_L, _L, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "bz_error_bounds": (_I, [_L, _P, _P, _P, _P, _P, _P, _P]),

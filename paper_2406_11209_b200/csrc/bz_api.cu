@@ -367,6 +367,13 @@ int bz_block_means(const bz_layout* L, const void* maxima, const void* indices, 
   return launch_block_means(make_geo(L), maxima, indices, out, S(stream));
 }
 
+int bz_block_means_dc(const bz_layout* L, const void* maxima, const void* dc, double* out,
+                      void* stream) {
+  if (int rc = validate(L)) return rc;
+  if (L->kept == 0 || !L->keeps_first) { set_error("block_means: mask drops the first coefficient"); return BZ_E_INVALID; }
+  return launch_block_means(make_geo(L), maxima, dc, out, S(stream), true);
+}
+
 size_t bz_wasserstein_workspace(const bz_layout* L) {
   if (validate(L)) return 0;
   return wasserstein_workspace(block_count(L));
@@ -381,6 +388,18 @@ int bz_approx_wasserstein(const bz_layout* La, const bz_layout* Lb, const void* 
   if (!La->keeps_first || !Lb->keeps_first || La->kept == 0 || Lb->kept == 0) { set_error("approx_wasserstein: mask drops the first coefficient"); return BZ_E_INVALID; }
   return launch_approx_wasserstein(make_geo(La), make_geo(Lb), a_max, a_idx, b_max, b_idx, order,
                                    tol, result, ws, ws_bytes, S(stream));
+}
+
+int bz_approx_wasserstein_dc(const bz_layout* La, const bz_layout* Lb, const void* a_max,
+                             const void* a_idx, const void* a_dc, const void* b_max,
+                             const void* b_idx, const void* b_dc, double order, double tol,
+                             double* result, void* ws, size_t ws_bytes, void* stream) {
+  if (int rc = validate(La)) return rc;
+  if (int rc = validate(Lb)) return rc;
+  if (block_count(La) != block_count(Lb)) { set_error("approx_wasserstein: block counts differ"); return BZ_E_INVALID; }
+  if (!La->keeps_first || !Lb->keeps_first || La->kept == 0 || Lb->kept == 0) { set_error("approx_wasserstein: mask drops the first coefficient"); return BZ_E_INVALID; }
+  return launch_approx_wasserstein(make_geo(La), make_geo(Lb), a_max, a_idx, b_max, b_idx, order,
+                                   tol, result, ws, ws_bytes, S(stream), a_dc, b_dc);
 }
 
 int bz_error_bounds(const bz_layout* L, const void* maxima, const void* indices,

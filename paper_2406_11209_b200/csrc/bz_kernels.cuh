@@ -66,11 +66,14 @@ int launch_dct4_decompress(const Geo& g, const void* maxima, const void* indices
 
 // block means / approximate Wasserstein distance (bz_wasserstein.cu)
 size_t wasserstein_workspace(int64_t nblocks);
+// dc_plane: `indices` is the contiguous DC plane (one index per block)
 int launch_block_means(const Geo& g, const void* maxima, const void* indices, double* out,
-                       cudaStream_t s);
+                       cudaStream_t s, bool dc_plane = false);
+// a_dc / b_dc: the operands' DC planes, or nullptr (K-strided gather of a_idx / b_idx)
 int launch_approx_wasserstein(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                               const void* b_max, const void* b_idx, double order, double tol,
-                              double* result, void* ws, size_t ws_bytes, cudaStream_t s);
+                              double* result, void* ws, size_t ws_bytes, cudaStream_t s,
+                              const void* a_dc = nullptr, const void* b_dc = nullptr);
 
 // error predictors (bz_metrics.cu)
 int launch_error_bounds(const Geo& g, const void* maxima, const void* indices,

@@ -24,13 +24,15 @@ constexpr int RED_CTAS = 296;     // partial-sum CTAs (fixed: deterministic)
 }  // namespace ws_
 
 // ------------------------------------------------------------ block means --
+// `stride` = kept (the K-strided first coefficients of the indices) or 1 (the
+// DC plane: indices[..., 0] stored contiguously by the producing kernel)
 template <typename IT>
-__global__ void k_block_means(int64_t nblocks, int kept, const void* __restrict__ maxima, int fk,
-                              const IT* __restrict__ indices, double r, double scale,
+__global__ void k_block_means(int64_t nblocks, int64_t stride, const void* __restrict__ maxima,
+                              int fk, const IT* __restrict__ indices, double r, double scale,
                               double* __restrict__ out) {
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblocks;
        b += (int64_t)gridDim.x * blockDim.x) {
-    const double f = (double)indices[b * (int64_t)kept];
+    const double f = (double)indices[b * stride];
     const double n = load_kind_rt(maxima, b, fk);
     // firsts = F0 * N; firsts /= r (ops.py:172-175); / block_mean_scale (ops.py:358)
     out[b] = __ddiv_rn(__ddiv_rn(__dmul_rn(f, n), r), scale);
@@ -66,15 +68,25 @@ __global__ void k_sum_max_partial(const double* __restrict__ a, const double* __
     for (int k = 0; k < 4; ++k) partial[blockIdx.x * 4 + k] = s[k][0];
 }
 
-// one CTA: stats = {sum a, max a, sum b, max b}
+// one CTA, one warp per statistic: stats = {sum a, max a, sum b, max b}.
+// Lane l sums partials l, l+32, ... in order, then a fixed xor tree: the same
+// bits every run (the single-thread sequential loop was a 300-deep chain of
+// dependent L2 loads, ~40 us)
 __global__ void k_sum_max_final(const double* __restrict__ partial, int nparts,
                                 double* __restrict__ stats) {
-  if (threadIdx.x < 4) {
-    const int k = threadIdx.x;
-    double v = (k & 1) ? -INFINITY : 0.0;
-    for (int i = 0; i < nparts; ++i) v = (k & 1) ? fmax(v, partial[i * 4 + k]) : v + partial[i * 4 + k];
-    stats[k] = v;
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (k >= 4) return;
+  double v = (k & 1) ? -INFINITY : 0.0;
+  for (int i = lane; i < nparts; i += 32) {
+    const double x = partial[i * 4 + k];
+    v = (k & 1) ? fmax(v, x) : v + x;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double y = __shfl_xor_sync(0xffffffffu, v, o);
+    v = (k & 1) ? fmax(v, y) : v + y;
+  }
+  if (lane == 0) stats[k] = v;
 }
 
 // softmax step 1 (ops.py:351-353): x <- exp(x - max) where |sum - 1| > tol
@@ -91,32 +103,37 @@ __global__ void k_softmax_exp(double* __restrict__ a, double* __restrict__ b, in
   }
 }
 
-// softmax step 2: x <- x / sum x (stats recomputed after step 1)
-__global__ void k_softmax_div(double* __restrict__ a, double* __restrict__ b, int64_t n,
-                              const double* __restrict__ stats, const int* __restrict__ flags) {
-  const bool fa = flags[0], fb = flags[1];
-  const double sa = stats[0], sb = stats[2];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (fa) a[i] = __ddiv_rn(a[i], sa);
-    if (fb) b[i] = __ddiv_rn(b[i], sb);
-  }
-}
-
 // ------------------------------------------------------------ radix sort --
 __device__ __forceinline__ unsigned long long key_of(double x) {
+  // order-preserving: negative -> ~u, otherwise u | sign.  The xor is inline
+  // PTX: written in C, nvcc turned `u | sign` of a computed double into the
+  // floating-point -|x| (DADD), which rewrites NaN payloads (a NaN then
+  // sorts below the positives instead of last)
   const unsigned long long u = (unsigned long long)__double_as_longlong(x);
-  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);  // order-preserving
+  const unsigned long long m = (unsigned long long)((long long)u >> 63) | 0x8000000000000000ull;
+  unsigned long long k;
+  asm("xor.b64 %0, %1, %2;" : "=l"(k) : "l"(u), "l"(m));
+  return k;
 }
 __device__ __forceinline__ double value_of(unsigned long long k) {
   const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double((long long)u);
 }
 
-__global__ void k_to_keys(const double* __restrict__ x, unsigned long long* __restrict__ k, int64_t n) {
+// softmax step 2: x <- x / sum x (stats recomputed after step 1), written
+// straight out as the sort keys (the keys replace the values in place)
+__global__ void k_softmax_div_keys(double* __restrict__ a, double* __restrict__ b, int64_t n,
+                                   const double* __restrict__ stats, const int* __restrict__ flags) {
+  const bool fa = flags[0], fb = flags[1];
+  const double sa = stats[0], sb = stats[2];
+  unsigned long long* ka = reinterpret_cast<unsigned long long*>(a);
+  unsigned long long* kb = reinterpret_cast<unsigned long long*>(b);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    k[i] = key_of(x[i]);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = a[i], y = b[i];
+    ka[i] = key_of(fa ? __ddiv_rn(x, sa) : x);
+    kb[i] = key_of(fb ? __ddiv_rn(y, sb) : y);
+  }
 }
 
 // Both distributions are sorted by the same launches: blockIdx.y selects the
@@ -289,11 +306,15 @@ __global__ void k_diff_pow_partial(const unsigned long long* __restrict__ ka,
   if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
 }
 
+// one warp: lane-strided partial sums in order, fixed xor tree
 __global__ void k_diff_pow_final(const double* __restrict__ partial, int nparts, int64_t n,
                                  double p, double* __restrict__ result) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int i = lane; i < nparts; i += 32) s += partial[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < nparts; ++i) s += partial[i];
     const double m = s / (double)n;
     result[0] = p == 1.0 ? m : pow(m, 1.0 / p);
   }
@@ -318,14 +339,15 @@ size_t wasserstein_workspace(int64_t nblocks) {
 }
 
 int launch_block_means(const Geo& g, const void* maxima, const void* indices, double* out,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool dc_plane) {
   const double r = radius_f64(g.index_kind), scale = sqrt((double)g.bsize);
+  const int64_t stride = dc_plane ? 1 : g.kept;
   const int grid = grid_for(g.nblocks, 256, 8);
   switch (g.index_kind) {
-    case BZ_I8: k_block_means<int8_t><<<grid, 256, 0, s>>>(g.nblocks, g.kept, maxima, g.float_kind, (const int8_t*)indices, r, scale, out); break;
-    case BZ_I16: k_block_means<int16_t><<<grid, 256, 0, s>>>(g.nblocks, g.kept, maxima, g.float_kind, (const int16_t*)indices, r, scale, out); break;
-    case BZ_I32: k_block_means<int32_t><<<grid, 256, 0, s>>>(g.nblocks, g.kept, maxima, g.float_kind, (const int32_t*)indices, r, scale, out); break;
-    default: k_block_means<int64_t><<<grid, 256, 0, s>>>(g.nblocks, g.kept, maxima, g.float_kind, (const int64_t*)indices, r, scale, out); break;
+    case BZ_I8: k_block_means<int8_t><<<grid, 256, 0, s>>>(g.nblocks, stride, maxima, g.float_kind, (const int8_t*)indices, r, scale, out); break;
+    case BZ_I16: k_block_means<int16_t><<<grid, 256, 0, s>>>(g.nblocks, stride, maxima, g.float_kind, (const int16_t*)indices, r, scale, out); break;
+    case BZ_I32: k_block_means<int32_t><<<grid, 256, 0, s>>>(g.nblocks, stride, maxima, g.float_kind, (const int32_t*)indices, r, scale, out); break;
+    default: k_block_means<int64_t><<<grid, 256, 0, s>>>(g.nblocks, stride, maxima, g.float_kind, (const int64_t*)indices, r, scale, out); break;
   }
   return check_launch("block_means");
 }
@@ -355,7 +377,8 @@ static int radix_sort2(unsigned long long* ka, unsigned long long* kb, unsigned 
 
 int launch_approx_wasserstein(const Geo& ga, const Geo& gb, const void* a_max, const void* a_idx,
                               const void* b_max, const void* b_idx, double order, double tol,
-                              double* result, void* ws, size_t ws_bytes, cudaStream_t s) {
+                              double* result, void* ws, size_t ws_bytes, cudaStream_t s,
+                              const void* a_dc, const void* b_dc) {
   const int64_t n = ga.nblocks;
   if (ws_bytes < wasserstein_workspace(n)) { set_error("approx_wasserstein: workspace too small"); return BZ_E_WORKSPACE; }
   unsigned char* p = reinterpret_cast<unsigned char*>(ws);
@@ -375,17 +398,15 @@ int launch_approx_wasserstein(const Geo& ga, const Geo& gb, const void* a_max, c
     k_diff_pow_final<<<1, 32, 0, s>>>(partial, 0, 0, order, result);
     return check_launch("wasserstein empty");
   }
-  if (int rc = launch_block_means(ga, a_max, a_idx, pa, s)) return rc;
-  if (int rc = launch_block_means(gb, b_max, b_idx, pb, s)) return rc;
+  if (int rc = launch_block_means(ga, a_max, a_dc ? a_dc : a_idx, pa, s, a_dc != nullptr)) return rc;
+  if (int rc = launch_block_means(gb, b_max, b_dc ? b_dc : b_idx, pb, s, b_dc != nullptr)) return rc;
   const int g = grid_for(n, ws_::RT, 8);
   k_sum_max_partial<<<ws_::RED_CTAS, ws_::RT, 0, s>>>(pa, pb, n, partial);
-  k_sum_max_final<<<1, 32, 0, s>>>(partial, ws_::RED_CTAS, stats);
+  k_sum_max_final<<<1, 128, 0, s>>>(partial, ws_::RED_CTAS, stats);
   k_softmax_exp<<<g, ws_::RT, 0, s>>>(pa, pb, n, stats, tol, flags);
   k_sum_max_partial<<<ws_::RED_CTAS, ws_::RT, 0, s>>>(pa, pb, n, partial);
-  k_sum_max_final<<<1, 32, 0, s>>>(partial, ws_::RED_CTAS, stats);
-  k_softmax_div<<<g, ws_::RT, 0, s>>>(pa, pb, n, stats, flags);
-  k_to_keys<<<g, ws_::RT, 0, s>>>(pa, ka, n);
-  k_to_keys<<<g, ws_::RT, 0, s>>>(pb, kb, n);
+  k_sum_max_final<<<1, 128, 0, s>>>(partial, ws_::RED_CTAS, stats);
+  k_softmax_div_keys<<<g, ws_::RT, 0, s>>>(pa, pb, n, stats, flags);
   if (int rc = check_launch("wasserstein prep")) return rc;
   if (int rc = radix_sort2(ka, kb, t1, t2, n, hist, csum, s)) return rc;
   k_diff_pow_partial<<<ws_::RED_CTAS, ws_::RT, 0, s>>>(ka, kb, n, order, partial);

@@ -646,8 +646,12 @@ def block_means(a: CompressedArray) -> torch.Tensor:
     _require_first_coefficient(a)
     out = torch.empty(a.block_count, dtype=torch.float64, device=a.device)
     La = a.layout()
-    _native.call("bz_block_means", ctypes.byref(La), a.maxima.data_ptr(), a.indices.data_ptr(),
-                 out.data_ptr(), _stream(a))
+    if a._dc is not None:  # the DC plane: B*(idx+f) contiguous bytes, no K-strided gather
+        _native.call("bz_block_means_dc", ctypes.byref(La), a.maxima.data_ptr(), a._dc.data_ptr(),
+                     out.data_ptr(), _stream(a))
+    else:
+        _native.call("bz_block_means", ctypes.byref(La), a.maxima.data_ptr(), a.indices.data_ptr(),
+                     out.data_ptr(), _stream(a))
     return out
 
 
@@ -675,8 +679,11 @@ def approx_wasserstein(a: CompressedArray, b: CompressedArray,
     bi = b.indices if b.device == dev else b.indices.to(dev)
     bm = b.maxima if b.device == dev else b.maxima.to(dev)
     res = torch.empty(1, dtype=torch.float64, device=dev)
-    _native.call("bz_approx_wasserstein", ctypes.byref(La), ctypes.byref(Lb), a.maxima.data_ptr(),
-                 a.indices.data_ptr(), bm.data_ptr(), bi.data_ptr(), float(params.order),
-                 float(params.normalization_tolerance), res.data_ptr(), ws.data_ptr(), ws.numel(),
-                 _stream(a))
+    # block means from the DC planes where the producing kernels wrote them
+    adc = a._dc.data_ptr() if a._dc is not None else None
+    bdc = b._dc.data_ptr() if b._dc is not None and b.device == dev else None
+    _native.call("bz_approx_wasserstein_dc", ctypes.byref(La), ctypes.byref(Lb),
+                 a.maxima.data_ptr(), a.indices.data_ptr(), adc, bm.data_ptr(), bi.data_ptr(), bdc,
+                 float(params.order), float(params.normalization_tolerance), res.data_ptr(),
+                 ws.data_ptr(), ws.numel(), _stream(a))
     return float(res.item())

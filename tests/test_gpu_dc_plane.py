@@ -163,3 +163,26 @@ def test_mean_plane_c3_size(bz):
     _plane_ok(cx)
     _plane_ok(t)
     _mean_both(bz, t)
+
+
+@pytest.mark.parametrize("case", [((40, 64, 48), (8, 8, 8), "f32", "i8"),
+                                  ((64, 96), (4, 4), "f64", "i16"),
+                                  ((16, 16, 16, 32), (4, 4, 4, 4), "f32", "i8")])
+def test_block_means_and_wasserstein_from_plane(bz, case):
+    """block_means / approx_wasserstein read the DC plane when the array has
+    one (bz_block_means_dc, bz_approx_wasserstein_dc): the same bits as the
+    K-strided gather of indices[..., 0] (ops.py:166-175, 355-384)."""
+    shape, block, fk, ik = case
+    rng = np.random.default_rng(7)
+    s = bz.CodecSettings(block, bz.FloatKind(fk), bz.IndexKind(ik))
+    dt = np.float32 if fk == "f32" else np.float64
+    xs = [rng.normal(size=shape).astype(dt) for _ in range(2)]
+    a, b = (bz.compress(bz.DenseArray(shape, bz.FloatKind(fk), x), s) for x in xs)
+    _plane_ok(a)
+    _plane_ok(b)
+    assert torch.equal(bz.block_means(a), bz.block_means(_strip(bz, a)))
+    for order in (1.0, 2.0, 1.5):
+        p = bz.ops.WassersteinParams(order=order)
+        w_plane = bz.approx_wasserstein(a, b, p)
+        assert w_plane == bz.approx_wasserstein(_strip(bz, a), _strip(bz, b), p)
+        assert w_plane == bz.approx_wasserstein(a, _strip(bz, b), p)
