@@ -116,7 +116,13 @@ k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
   };
   fetch(group);
 
-  for (int64_t b = group; b < nblocks; b += ngroups) {
+  // warp-uniform trip count (the warp's first group decides): every lane runs
+  // every iteration, so the group maximum and vote below are full-warp
+  // collectives; a group past the end computes on stale registers and stores
+  // nothing (a partial-mask vote compiled to WARPSYNC.EXCLUSIVE, one vote per
+  // group in turn)
+  for (int64_t b = group; b - lane / GS < nblocks; b += ngroups) {
+    const bool active = b < nblocks;
     const int64_t base = b * (int64_t)kept;
     uint4 ca[NCH], cb[NCH];
 #pragma unroll
@@ -167,7 +173,7 @@ k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
     m = m23 > m ? m23 : m;
 #pragma unroll
     for (int o = GS / 2; o > 0; o >>= 1) {
-      const double t = __shfl_xor_sync(gmask, m, o, GS);
+      const double t = __shfl_xor_sync(0xffffffffu, m, o, GS);
       m = t > m ? t : m;
     }
     const double n = round_to_kind<BZ_F32>(m);
@@ -194,7 +200,8 @@ k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
     }
     const bool near = min(min(z4[0], z4[1]), min(z4[2], z4[3])) < kNearHalf;
     const bool bad = !safe || !bc.fast || !(m < 1.7976931348623157e308);
-    const bool any_bad = (__ballot_sync(gmask, near || bad) & gmask) != 0u;
+    const bool any_bad = (__ballot_sync(0xffffffffu, active && (near || bad)) & gmask) != 0u;
+    if (!active) continue;
     if (!any_bad) {
       if constexpr (RED) {
         int sq = 0;  // <= 32 * 127^2 per chunk: exact in int32

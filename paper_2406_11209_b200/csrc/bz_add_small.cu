@@ -145,7 +145,14 @@ k_add_small(int64_t nblocks, int kept, const float* __restrict__ a_max,
     const unsigned char* sb = cur + IB;
     const float* sma = reinterpret_cast<const float*>(cur + 2 * IB);
     const float* smb = sma + TBS;
-    for (int lb = t / G; lb < nv; lb += 256 / G) {
+    // warp-uniform trip count: every lane of a warp runs every iteration (a
+    // group past the tile's last block computes on stale shared bytes --
+    // lb < TBS -- and stores nothing), so the group votes and shuffles are
+    // full-warp (a partial-mask vote serialised the 8 groups of a warp:
+    // WARPSYNC.EXCLUSIVE + 8 votes per block)
+    for (int lw = (t / 32) * (32 / G); lw < nv; lw += 256 / G) {
+      const int lb = lw + lane / G;
+      const bool active = lb < nv;
       const int64_t b = b0 + lb;
       const int8_t* pa = reinterpret_cast<const int8_t*>(sa) + lb * kept;
       const int8_t* pb = reinterpret_cast<const int8_t*>(sb) + lb * kept;
@@ -185,7 +192,7 @@ k_add_small(int64_t nblocks, int kept, const float* __restrict__ a_max,
       double m = CPL > 1 ? (fabs(m2[1]) > fabs(m2[0]) ? fabs(m2[1]) : fabs(m2[0])) : fabs(m2[0]);
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) {
-        const double x = __shfl_xor_sync(gmask, m, o, G);
+        const double x = __shfl_xor_sync(0xffffffffu, m, o, G);
         m = x > m ? x : m;
       }
       const double n = round_to_kind<BZ_F32>(m);
@@ -198,8 +205,10 @@ k_add_small(int64_t nblocks, int kept, const float* __restrict__ a_max,
         hb[j] = (unsigned)__double2hiint(d);
         z = min(z, (unsigned)__double2loint(d));
       }
-      const bool bad = !safe || !bc.fast || !(m < 1.7976931348623157e308) || z < kNearHalf;
-      if ((__ballot_sync(gmask, bad) & gmask) == 0u) {
+      const bool bad = active && (!safe || !bc.fast || !(m < 1.7976931348623157e308) || z < kNearHalf);
+      const unsigned vote = __ballot_sync(0xffffffffu, bad) & gmask;
+      if (!active) continue;  // (after the warp's last collective of the iteration)
+      if (vote == 0u) {
         if (RED) {
           int sq = 0;
 #pragma unroll
