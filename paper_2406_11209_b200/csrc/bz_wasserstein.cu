@@ -148,9 +148,18 @@ k_radix_hist(const unsigned long long* __restrict__ keys0, const unsigned long l
   h[threadIdx.x] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * ws_::RT * rounds;
-  for (int rr = 0; rr < rounds; ++rr) {
+  // every round's key is loaded before the first is counted: one DRAM latency
+  // per tile instead of one per round
+  unsigned long long k[ws_::MAX_ROUNDS];
+#pragma unroll
+  for (int rr = 0; rr < ws_::MAX_ROUNDS; ++rr) {
     const int64_t i = base + rr * ws_::RT + threadIdx.x;
-    if (i < n) atomicAdd(&h[(unsigned)(keys[i] >> shift) & 255u], 1u);
+    k[rr] = (rr < rounds && i < n) ? __ldcs(keys + i) : ~0ull;
+  }
+#pragma unroll
+  for (int rr = 0; rr < ws_::MAX_ROUNDS; ++rr) {
+    const int64_t i = base + rr * ws_::RT + threadIdx.x;
+    if (rr < rounds && i < n) atomicAdd(&h[(unsigned)(k[rr] >> shift) & 255u], 1u);
   }
   __syncthreads();
   hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
@@ -244,7 +253,29 @@ __global__ void __launch_bounds__(1024) k_scan_down(unsigned* __restrict__ v, in
   }
 }
 
-// stable scatter: keys of tile `blockIdx.x` to their global positions
+// lanes of the warp holding the same 8-bit digit (bit-sliced ballots: eight
+// votes instead of a MATCH.ANY); d >= 256 marks an invalid lane, which then
+// matches only other invalid lanes
+__device__ __forceinline__ unsigned digit_peers(unsigned d) {
+  unsigned m = __ballot_sync(0xffffffffu, d < 256u);
+  if (d >= 256u) m = ~m;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const unsigned v = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+    m &= ((d >> b) & 1u) ? v : ~v;
+  }
+  return m;
+}
+
+// stable scatter: keys of tile `blockIdx.x` to their global positions.  Warp
+// w owns the tile's keys [w*32*rounds, (w+1)*32*rounds) (its rounds of 32
+// consecutive keys, held in registers); pass 1 counts each warp's digits,
+// one CTA-wide exclusive scan over the warps turns the counts into per-warp
+// running positions, pass 2 writes every round's keys at position + rank
+// among equal digits (bit-sliced votes).  Two CTA barriers per tile (the
+// per-round CTA-wide ranking used three per 256 keys: C3 47 -> 43 us per
+// pass; a variant that sorts the tile in shared memory first and writes
+// digit runs measured 47 us -- the scattered 8-byte stores are not the limit).
 __global__ void __launch_bounds__(ws_::RT)
 k_radix_scatter(const unsigned long long* __restrict__ in0, const unsigned long long* __restrict__ in1,
                 unsigned long long* __restrict__ out0, unsigned long long* __restrict__ out1,
@@ -253,36 +284,49 @@ k_radix_scatter(const unsigned long long* __restrict__ in0, const unsigned long 
   const unsigned long long* __restrict__ in = blockIdx.y ? in1 : in0;
   unsigned long long* __restrict__ out = blockIdx.y ? out1 : out0;
   offsets += (int64_t)blockIdx.y * 256 * ntiles;
-  __shared__ unsigned int run[256];
-  __shared__ unsigned int wcnt[ws_::RT / 32][256];
+  constexpr int NW = ws_::RT / 32;
+  __shared__ unsigned int cnt[NW][256];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  run[t] = offsets[(int64_t)t * ntiles + blockIdx.x];
-  for (int k = 0; k < ws_::RT / 32; ++k) wcnt[k][t] = 0;
+#pragma unroll
+  for (int k = 0; k < NW; ++k) cnt[k][t] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * ws_::RT * rounds;
+  const int64_t wbase = (int64_t)blockIdx.x * ws_::RT * rounds + (int64_t)w * 32 * rounds;
   const unsigned lt = (1u << lane) - 1u;
-  for (int rr = 0; rr < rounds; ++rr) {
-    const int64_t i = base + rr * ws_::RT + t;
-    const bool valid = i < n;
-    const unsigned long long key = valid ? in[i] : 0ull;
-    const unsigned d = valid ? ((unsigned)(key >> shift) & 255u) : 256u;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    const unsigned lrank = __popc(peers & lt);
-    if (valid && lrank == 0) wcnt[w][d] = __popc(peers);
-    __syncthreads();
-    if (valid) {
-      unsigned pre = 0;
-      for (int w2 = 0; w2 < w; ++w2) pre += wcnt[w2][d];
-      out[run[d] + pre + lrank] = key;
-    }
-    __syncthreads();
-    unsigned tot = 0;
-    for (int k = 0; k < ws_::RT / 32; ++k) {
-      tot += wcnt[k][t];
-      wcnt[k][t] = 0;
-    }
-    run[t] += tot;
-    __syncthreads();
+  unsigned long long kr[ws_::MAX_ROUNDS];
+#pragma unroll
+  for (int rr = 0; rr < ws_::MAX_ROUNDS; ++rr) {
+    const int64_t i = wbase + rr * 32 + lane;
+    kr[rr] = (rr < rounds && i < n) ? __ldcs(in + i) : 0ull;
+  }
+#pragma unroll
+  for (int rr = 0; rr < ws_::MAX_ROUNDS; ++rr) {
+    if (rr >= rounds) break;
+    const bool valid = wbase + rr * 32 + lane < n;
+    const unsigned d = valid ? ((unsigned)(kr[rr] >> shift) & 255u) : 256u;
+    const unsigned peers = digit_peers(d);
+    if (valid && (peers & lt) == 0u) cnt[w][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  unsigned run = offsets[(int64_t)t * ntiles + blockIdx.x];  // thread t = digit t
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    const unsigned c = cnt[k][t];
+    cnt[k][t] = run;
+    run += c;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int rr = 0; rr < ws_::MAX_ROUNDS; ++rr) {
+    if (rr >= rounds) break;
+    const bool valid = wbase + rr * 32 + lane < n;
+    const unsigned d = valid ? ((unsigned)(kr[rr] >> shift) & 255u) : 256u;
+    const unsigned peers = digit_peers(d);
+    const unsigned pos = valid ? cnt[w][d] : 0u;
+    if (valid) out[pos + __popc(peers & lt)] = kr[rr];
+    __syncwarp();
+    if (valid && (peers & lt) == 0u) cnt[w][d] = pos + __popc(peers);
+    __syncwarp();
   }
 }
 
