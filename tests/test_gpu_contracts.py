@@ -113,6 +113,7 @@ def test_reductions_with_all_false_mask(bz, rng):
     assert a.indices.shape == (2, 2, 0)
     assert bz.l2_norm(a) == 0.0
     assert bz.dot(a, a) == 0.0
+    assert bz.subtract_l2(a, a) == 0.0  # no kept coefficient: the empty-case store
     with pytest.raises(bz.errors.ZeroNormOperand):
         bz.cosine_similarity(a, a)
     assert int(torch.count_nonzero(bz.decompress(a).values).item()) == 0
@@ -240,14 +241,18 @@ def test_concurrent_reductions_from_threads(bz):
     s = bz.CodecSettings((8, 8, 8), bz.FloatKind.F32, bz.IndexKind.I8)
     arrs = [bz.compress(bz.DenseArray.of(rng.normal(size=(64, 64, 64)), bz.FloatKind.F32), s)
             for _ in range(4)]
-    serial = [(bz.dot(arrs[i], arrs[(i + 1) % 4]), bz.l2_norm(arrs[i])) for i in range(4)]
+    def ops3(i):  # subtract_l2's last CTA writes into the calling thread's pinned record
+        return (bz.dot(arrs[i], arrs[(i + 1) % 4]), bz.l2_norm(arrs[i]),
+                bz.subtract_l2(arrs[i], arrs[(i + 1) % 4]))
+
+    serial = [ops3(i) for i in range(4)]
     errors, results = [], {}
 
     def worker(i):
         try:
             got = []
             for _ in range(50):
-                got.append((bz.dot(arrs[i], arrs[(i + 1) % 4]), bz.l2_norm(arrs[i])))
+                got.append(ops3(i))
             results[i] = got
         except Exception as e:  # pragma: no cover
             errors.append(e)
