@@ -34,6 +34,8 @@ def main(name, reps=2):
                "cov": lambda: bz.ops.moments_record(ca, cb),
                "mean": lambda: bz.ops.moments_record(ca, dc_only=True),
                "add": lambda: bz.add(ca, cb),
+               "dec": lambda: bz.decompress(ca),
+               "comp": lambda: bz.compress(x, s),
                "sub_l2": lambda: bz.ops._subtract_l2_sq(
                    ca, cb, torch.empty(1, dtype=torch.float64, device=ca.device))}
         for _ in range(reps):
