@@ -63,9 +63,14 @@ __device__ __forceinline__ Scale make_scale(double n, int fk) {
   return s;
 }
 __device__ __forceinline__ double fn_product(int f, const Scale& s) {
-  const double biased = __hiloint2double(0x43300000, (int)((unsigned)f ^ 0x80000000u));
-  if (s.narrow) return __fma_rn(biased, s.n, s.nbias);
-  return __dmul_rn(biased - 4503601774854144.0, s.n);
+  if (s.narrow) {
+    const double biased = __hiloint2double(0x43300000, (int)((unsigned)f ^ 0x80000000u));
+    return __fma_rn(biased, s.n, s.nbias);
+  }
+  // wide (F64) maxima: one int -> f64 conversion (the conversion unit has
+  // room here) instead of the bias form's constant move, xor and DADD --
+  // k_add at C2 is issue-bound
+  return __dmul_rn((double)f, s.n);
 }
 __device__ __forceinline__ double fn_product(long long f, const Scale& s) {
   return __dmul_rn((double)f, s.n);
