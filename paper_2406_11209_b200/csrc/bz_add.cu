@@ -258,13 +258,30 @@ k_add(int64_t nblocks, int kept, int fk_a, int fk_b, int fk_out,
     const double mx = __longlong_as_double((long long)key);  // NaN-propagating via bit order
     const double n = rnd_max<FK>(mx, fk_out);
     if (!RED && sub == 0) st_max<FK>(out_max, b, n, fk_out);
-    const BinCtx bc = bin_ctx(n, r, mx);
+    // 16-bit indices under F64 / F32 maxima (stored maximum within 2^-20 of
+    // the true one: no clamp) bin through kMagicH (bz_common.cuh): the index
+    // is the high word's low half, the low word the near-half test -- one
+    // DFMA and a min per coefficient (C2: k_add is issue-bound)
+    constexpr bool MAGIC16 = sizeof(IT) == 2 && (FK == BZ_F64 || FK == BZ_F32);
+    const BinCtx bc = bin_ctx<!MAGIC16>(n, r, mx);
     long long red_sq = 0;  // RED: this lane's exact sum of q^2 over the block
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       const int k0 = (ch * GS + sub) * V;
       int q[V];
-      if constexpr (sizeof(IT) <= 2) {
+      if constexpr (MAGIC16) {
+        unsigned z = 0xffffffffu;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const double d = __fma_rn(c[ch * V + e], bc.R, kMagicH);
+          q[e] = (int)(short)__double2hiint(d);
+          z = min(z, (unsigned)__double2loint(d));
+        }
+        if ((z < kNearHalf) | !bc.fast) {
+#pragma unroll
+          for (int e = 0; e < V; ++e) q[e] = (int)bin_exact_ctx(c[ch * V + e], bc, r, r);
+        }
+      } else if constexpr (sizeof(IT) <= 2) {
         unsigned nacc = 0;
 #pragma unroll
         for (int e = 0; e < V; ++e) q[e] = fast_index32<IT, true>(c[ch * V + e], bc.R, (int)r, nacc);
