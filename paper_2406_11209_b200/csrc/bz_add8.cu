@@ -145,39 +145,43 @@ k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
       if (subtract) { thb = -thb; tlb = -tlb; }
     }
     double c[L];
-    double m4[4];
+    // block maximum in float32: RN32 is monotone, so the largest RN32(|c|)
+    // is RN32(max |c|) -- exactly the stored maximum N (round_to_kind<F32>)
+    // -- for one conversion and a 3-input FMNMX per coefficient instead of
+    // a DSETP + 2 FSEL compare-select chain, and one 32-bit shuffle per
+    // step; an N that is not a normal float goes to the exact path
+    float mf[2] = {0.f, 0.f};
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       const uint32_t wa[4] = {ca[ch].x, ca[ch].y, ca[ch].z, ca[ch].w};
-      const uint32_t wb[4] = {cb[ch].x, cb[ch].y, cb[ch].z, cb[ch].w};
+      // operand b's bytes as unsigned (f + 128): its f64 values come from the
+      // bias form 2^52 + (f + 128) - (2^52 + 128) on the FP64 pipe, which
+      // keeps the 16-per-clock conversion unit at two operations per
+      // coefficient (a's int8 -> f64 and the float32 maximum)
+      const uint32_t wb[4] = {cb[ch].x ^ 0x80808080u, cb[ch].y ^ 0x80808080u,
+                              cb[ch].z ^ 0x80808080u, cb[ch].w ^ 0x80808080u};
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const double fa = (double)(int)(int8_t)(wa[e >> 2] >> (8 * (e & 3)));
         double cc = __fma_rn(fa, tha, fa * tla);
         if (MODE == 0) {
-          const double fb = (double)(int)(int8_t)(wb[e >> 2] >> (8 * (e & 3)));
+          const double fb =
+              __hiloint2double(0x43300000, (int)__byte_perm(wb[e >> 2], 0u, 0x4440 + (e & 3))) -
+              4503599627370624.0;  // 2^52 + 128
           cc = __dadd_rn(cc, __fma_rn(fb, thb, fb * tlb));
         } else if (ch == 0 && e == 0) {
           if (sub == 0) cc = __dadd_rn(cc, shift);
         }
         c[ch * 16 + e] = cc;
-        // chunks past `kept` hold zeros: they cannot raise the maximum; the
-        // chains start from real elements (from 0.0 the compiler assumes a
-        // non-negative running value and drops the |.| -- see bz_dct8.cu)
-        if (ch == 0 && e < 4) m4[e] = cc;
-        else m4[e & 3] = fabs(cc) > fabs(m4[e & 3]) ? cc : m4[e & 3];
+        // chunks past `kept` hold zeros: they cannot raise the maximum
+        mf[e & 1] = fmaxf(mf[e & 1], __double2float_rn(fabs(cc)));
       }
     }
-    double m = fabs(m4[0]) > fabs(m4[1]) ? fabs(m4[0]) : fabs(m4[1]);
-    const double m23 = fabs(m4[2]) > fabs(m4[3]) ? fabs(m4[2]) : fabs(m4[3]);
-    m = m23 > m ? m23 : m;
+    float nf = fmaxf(mf[0], mf[1]);
 #pragma unroll
-    for (int o = GS / 2; o > 0; o >>= 1) {
-      const double t = __shfl_xor_sync(0xffffffffu, m, o, GS);
-      m = t > m ? t : m;
-    }
-    const double n = round_to_kind<BZ_F32>(m);
-    const BinCtx bc = bin_ctx<false>(n, r, m);
+    for (int o = GS / 2; o > 0; o >>= 1) nf = fmaxf(nf, __shfl_xor_sync(0xffffffffu, nf, o, GS));
+    const double n = (double)nf;
+    const BinCtx bc = bin_ctx<false>(n, r, n);
     // 32-bit fixed point (kMagicH, bz_common.cuh): index = low byte of the
     // high word unless the fraction (low word) is within 2^-24 of one half
     unsigned z4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
@@ -199,7 +203,7 @@ k_add8(int64_t nblocks, int kept, const float* __restrict__ a_max,
       ov[ch] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     }
     const bool near = min(min(z4[0], z4[1]), min(z4[2], z4[3])) < kNearHalf;
-    const bool bad = !safe || !bc.fast || !(m < 1.7976931348623157e308);
+    const bool bad = !safe || !bc.fast || !(nf >= 1.17549435e-38f && nf <= 3.40282347e+38f);
     const bool any_bad = (__ballot_sync(0xffffffffu, active && (near || bad)) & gmask) != 0u;
     if (!active) continue;
     if (!any_bad) {
