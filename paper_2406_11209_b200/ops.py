@@ -549,6 +549,7 @@ def ssim(a: CompressedArray, b: CompressedArray, params: SsimParams | None = Non
 
 # ------------------------------------------------ time-series workflow --
 _SL2_WS: dict = {}
+_SL2_BYTES: list = []  # bz_subtract_l2_workspace(): a library constant, queried once
 
 
 @_native.on_device
@@ -559,7 +560,9 @@ def _subtract_l2_sq(a: CompressedArray, b: CompressedArray, out: torch.Tensor) -
     _check_compatible(a, b, index_kind=True)
     dev = a.device
     key = (dev.index, _native.stream_handle(dev))
-    nbytes = _native.query("bz_subtract_l2_workspace")
+    if not _SL2_BYTES:
+        _SL2_BYTES.append(int(_native.query("bz_subtract_l2_workspace")))
+    nbytes = _SL2_BYTES[0]
     ws = _SL2_WS.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
@@ -573,6 +576,7 @@ def _subtract_l2_sq(a: CompressedArray, b: CompressedArray, out: torch.Tensor) -
     if rc == -2:  # BZ_E_UNSUPPORTED
         return False
     if rc != 0:
+        ws.zero_()  # never leave a half-counted ticket behind a failed launch
         raise _native.NativeError(f"bz_subtract_l2 failed ({rc}): "
                                   f"{_native.load_library().bz_last_error().decode()}")
     return True
