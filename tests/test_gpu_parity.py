@@ -593,3 +593,36 @@ def test_add8_large_array_group_width(bz):
         assert np.array_equal(gi, want.indices.reshape(-1, keep))
     fused, ref = bz.subtract_l2(a, b), bz.l2_norm(bz.subtract(a, b))
     assert math.isclose(fused, ref, rel_tol=1e-12), (fused, ref)
+
+
+@pytest.mark.parametrize("fk", ["f64", "f32"])
+def test_add_rebinning_exact_halves(bz, fk):
+    """16-bit rebinning on exact and near rounding halves (k_add's kMagicH
+    path hands them to the exact binning): blocks whose sums rebin to
+    +-r/2 and (2j+1)/2 positions, ties-to-even as the reference
+    (codec.py:272-277, ops.py:178-204); bit-exact with the oracle for add,
+    subtract, add_scalar and the fused subtract+l2."""
+    rng = np.random.default_rng(11)
+    block, grid = (4, 4), (24, 16)
+    shape = (block[0] * grid[0], block[1] * grid[1])
+    nb = grid[0] * grid[1]
+    fmax = 2 * rng.integers(1, 16383, size=nb)
+    fa = rng.integers(-1, 2, size=(nb, 16)) * (fmax[:, None] // 2)
+    fa[:, 0] = fmax
+    fa[:, 5:] = rng.integers(-fmax[:, None] // 2, fmax[:, None] // 2 + 1, size=(nb, 11))
+    fb = np.where(rng.random((nb, 16)) < 0.5, 0, rng.integers(-3, 4, size=(nb, 16)))
+    fb[:, 0] = 0
+    na = rng.choice([1.0, 0.75, 3.0, 2.0 ** -20], size=nb)
+    nbm = np.where(rng.random(nb) < 0.5, na, rng.choice([1.0, 0.5, 6.0], size=nb))
+    s = _settings(bz, block, fk, "i16")
+    os_ = o.Settings(block, fk, "i16", "dct")
+    ra = o.Compressed(shape, os_, na.reshape(grid), fa.reshape(grid + (16,)).astype(np.int16))
+    rb = o.Compressed(shape, os_, nbm.reshape(grid), fb.reshape(grid + (16,)).astype(np.int16))
+    a = bz.CompressedArray(shape, s, ra.maxima, ra.indices)
+    b = bz.CompressedArray(shape, s, rb.maxima, rb.indices)
+    for got, want in ((bz.add(a, b), o.add(ra, rb)), (bz.subtract(a, b), o.subtract(ra, rb)),
+                      (bz.add_scalar(a, 0.5), o.add_scalar(ra, 0.5))):
+        assert np.array_equal(got.maxima_f64().cpu().numpy(), want.maxima)
+        assert np.array_equal(got.indices.cpu().numpy(), want.indices)
+    want_l2 = o.l2_norm(o.subtract(ra, rb))
+    assert bz.subtract_l2(a, b) == pytest.approx(want_l2, rel=1e-12)
