@@ -626,3 +626,31 @@ def test_add_rebinning_exact_halves(bz, fk):
         assert np.array_equal(got.indices.cpu().numpy(), want.indices)
     want_l2 = o.l2_norm(o.subtract(ra, rb))
     assert bz.subtract_l2(a, b) == pytest.approx(want_l2, rel=1e-12)
+
+
+def test_add8_float32_maximum_edges(bz):
+    """add8 (int8 indices, F32 maxima, 8^3 blocks) takes the block maximum
+    in float32 (max RN32|c| = RN32 max|c|): exact halves, sums whose maximum
+    rounds to an f32 subnormal or overflows (exact path), zero blocks --
+    bit-exact with the oracle (ops.py:178-204)."""
+    rng = np.random.default_rng(12)
+    block, grid = (8, 8, 8), (6, 4, 4)
+    shape = tuple(b * g for b, g in zip(block, grid))
+    nb, K = int(np.prod(grid)), 512
+    fa = rng.integers(-127, 128, size=(nb, K))
+    fa[:, 0] = 126
+    fa[:, 1] = 63  # 63/126 * 127 = 63.5: an exact half
+    fb = np.where(rng.random((nb, K)) < 0.7, 0, rng.integers(-2, 3, size=(nb, K)))
+    na = rng.choice([1.0, 0.375, 1e-39, 3e38, 2.0 ** -126], size=nb).astype(np.float32).astype(np.float64)
+    nbm = np.where(rng.random(nb) < 0.5, na, 1.0)
+    fa[-1] = 0
+    fb[-1] = 0  # an all-zero block
+    s = _settings(bz, block, "f32", "i8")
+    os_ = o.Settings(block, "f32", "i8", "dct")
+    ra = o.Compressed(shape, os_, na.reshape(grid), fa.reshape(grid + (K,)).astype(np.int8))
+    rb = o.Compressed(shape, os_, nbm.reshape(grid), fb.reshape(grid + (K,)).astype(np.int8))
+    a = bz.CompressedArray(shape, s, ra.maxima, ra.indices)
+    b = bz.CompressedArray(shape, s, rb.maxima, rb.indices)
+    for got, want in ((bz.add(a, b), o.add(ra, rb)), (bz.subtract(a, b), o.subtract(ra, rb))):
+        assert np.array_equal(got.maxima_f64().cpu().numpy(), want.maxima)
+        assert np.array_equal(got.indices.cpu().numpy(), want.indices)
